@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""HASF throughput bench (BASELINE.json metric: images/s on a 512^2 batch,
+% of the HBM roofline, vs the CPU reference).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c1] [--impl ours|reference]
+
+Default workload = config c1 (256 x 512x512 synthetic blob images, r = 1..5,
+(8,4)).  A step = one hasf_batch over the rank's whole batch, inputs already
+resident in HBM (value); e2e = the same through the C ABI's host-buffer entry
+(ts_hasf_batch_host: pinned host -> device copy, kernel, device -> host copy
+inside the timed region).  Multi-GPU (torchrun): every rank smooths its own
+256 distinct images (weak scaling, no data-path collective); time = max over
+ranks.  --impl reference times the CPU restatement of the reference (oracle/,
+all host threads) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1603_09337_b200 import workloads as W  # noqa: E402
+
+METRIC = "HASF images/s (512^2 batch, 1 B200), % HBM roofline, vs CPU ref"
+PAPER_CPU_IMG_S = 32.0   # PAPER.md:13,330 (2x Xeon E5405, unknown r / images): context only
+
+
+def bytes_per_image(cfg) -> int:
+    """SURVEY §8(d) contract: 8 stages per radius x 4 B/px."""
+    return 32 * cfg.r_max * cfg.h * cfg.w
+
+
+def peak_hbm():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(cfg_name):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(cfg_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(cfg, images, threads):
+    import oracle as O
+    t0 = time.perf_counter()
+    O.hasf_batch(images, cfg.r_max, cfg.fg, threads=threads)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    sample_n = max(1, min(cfg.n, cores * 2 if cfg.h * cfg.w <= 512 * 512 else cores))
+    imgs = W.config_batch(cfg, 0, sample_n)
+    for _ in range(args.warmup):
+        cpu_reference(cfg, imgs[:min(sample_n, cores)], cores)
+    t = 0.0
+    for _ in range(args.steps):
+        t += cpu_reference(cfg, imgs, cores)
+    value = args.steps * sample_n / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (SURVEY §8d generator, per-image seeds)",
+        "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.h}x{cfg.w} r_max={cfg.r_max} "
+                               f"({cfg.fg},{12 - cfg.fg})", "sample_images_per_step": sample_n},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample_n} images of {cfg.name} per step, oracle/ C restatement of the "
+                                   f"reference (hasf, smoothing.py:187-212) on {cores} host threads"},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c1", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=0, help="override images per rank")
+    ap.add_argument("--smem-budget", type=int, default=-1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="default: = steps")
+    ap.add_argument("--verify", type=int, default=2, help="images checked bit-exact vs the oracle")
+    args = ap.parse_args()
+    cfg = W.CONFIGS[args.config]
+    if args.batch > 0:
+        cfg = W.Config(**{**cfg.__dict__, "n": args.batch})
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1603_09337_b200 as P
+    from paper_1603_09337_b200 import _lib
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    if args.smem_budget >= 0:
+        _lib.load().ts_set_smem_budget(args.smem_budget)
+    adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
+
+    # this rank's images: indices rank*n .. rank*n + n - 1 (distinct seeds, weak scaling)
+    imgs_np = W.config_batch(cfg, rank * cfg.n, cfg.n)
+    x = torch.from_numpy(imgs_np).cuda()
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    lib = _lib.load()
+
+    def step():
+        _lib.check(lib.ts_hasf_batch(x.data_ptr(), out.data_ptr(), cfg.n, cfg.h, cfg.w, cfg.r_max, cfg.fg,
+                                     None, None, stream.cuda_stream, None))
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)          # evict L2 between timed steps (not timed)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    total_images = cfg.n * world * args.steps
+    value = total_images / (t_ms / 1e3)
+
+    # stats + correctness sample (outside the timed region)
+    _, stats = P.hasf_batch(x, cfg.r_max, adj, stats=True)
+    verified = 0
+    if args.verify > 0 and rank == 0:
+        import oracle as O
+        k = min(args.verify, cfg.n)
+        want = O.hasf_batch(imgs_np[:k], cfg.r_max, cfg.fg)
+        assert np.array_equal(out[:k].cpu().numpy(), want), "bench output differs from the oracle"
+        verified = k
+
+    # e2e through the C ABI host-buffer entry, pinned host memory
+    e2e_steps = args.e2e_steps or args.steps
+    hin = torch.from_numpy(imgs_np).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+
+    def e2e_step():
+        _lib.check(lib.ts_hasf_batch_host(hin.data_ptr(), hout.data_ptr(), cfg.n, cfg.h, cfg.w, cfg.r_max,
+                                          cfg.fg, None, None, stream.cuda_stream))
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_end)
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    assert np.array_equal(hout.numpy(), out.cpu().numpy())
+    e2e_value = cfg.n * world * e2e_steps / (e2e_ms / 1e3)
+
+    if rank == 0:
+        peak, peak_src = peak_hbm()
+        bpi = bytes_per_image(cfg)
+        kernel_s = t_ms / 1e3 / args.steps          # one fused launch per step
+        achieved = bpi * cfg.n / kernel_s / 1e9
+        cpu = None
+        if not args.no_cpu_baseline and world >= 1:
+            cores = os.cpu_count() or 1
+            sample_n = min(cfg.n, cores * 2 if cfg.h * cfg.w <= 512 * 512 else max(1, cores // 2))
+            ts_ = cpu_reference(cfg, imgs_np[:sample_n], cores)
+            cpu = {"value": sample_n / ts_, "unit": "images/s", "cores": cores, "kind": "port",
+                   "sample": f"{sample_n} images of {cfg.name} ({cfg.h}x{cfg.w}, r_max={cfg.r_max}), oracle/ C "
+                             f"restatement of the reference hasf on {cores} host threads, {ts_:.1f} s"}
+        plan = np.zeros(5, np.int64)
+        lib.ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
+        line = {
+            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (SURVEY §8d generator, per-image seeds; paper images not shipped)",
+            "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.h}x{cfg.w} per GPU, r_max={cfg.r_max}, "
+                                   f"({cfg.fg},{12 - cfg.fg})", "global_batch": cfg.n * world,
+                       "image": [cfg.h, cfg.w], "r_max": cfg.r_max, "adjacency": [cfg.fg, 12 - cfg.fg],
+                       "parallelism": f"images sharded over {world} GPU(s), no collective",
+                       "l2": "flushed between timed steps (256 MiB fill, not timed); per-step CUDA events",
+                       "plan": {"ctas_per_wave": int(plan[0]), "ctas_per_sm": int(plan[1]),
+                                "smem_bytes": int(plan[2]), "smem_mask": int(plan[3]),
+                                "gws_bytes_per_cta": int(plan[4])}},
+            "mpix_per_s": value * cfg.h * cfg.w / 1e6,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic_from_profiles(cfg.name),
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": bpi * cfg.n,
+                         "bytes_model": "32*r_max*H*W per image (SURVEY §8d: 8 stages/radius x 4 B/px)",
+                         "kernel": "ts::hasf_kernel (one launch per step)"},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": cfg.n * cfg.h * cfg.w,
+                    "d2h_bytes_per_step": cfg.n * cfg.h * cfg.w, "wall_ms": wall_ms,
+                    "path": "ts_hasf_batch_host (C ABI, pinned host buffers)"},
+            "gpu_launches": args.steps,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "engine_stats_per_image": {"sweeps": float(stats[:, 0].mean()), "fixpoint_passes": float(stats[:, 1].mean()),
+                                       "engine_calls": float(stats[:, 2].mean()), "flips": float(stats[:, 3].mean())},
+            "verified_images_vs_oracle": verified,
+            "step_ms": step_ms,
+            "paper_cpu_context_img_s": PAPER_CPU_IMG_S,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

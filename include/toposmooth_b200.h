@@ -1,0 +1,135 @@
+/*
+ * toposmooth_b200 -- C ABI of the B200-native HASF path (sm_100a).
+ *
+ * Drop-in boundary for the reference's public Python API (toposmooth, which
+ * has no native FFI of its own: its kernels are numba functions taking numpy
+ * arrays by reference and writing preallocated outputs, e.g.
+ * _phase1_kernel(pix, g, cols, inf, invert), edt.py:46).  Each entry point
+ * below names the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/toposmooth/).
+ *
+ * Conventions
+ *  - Images are uint8 {0,1}, row-major [n][h][w] batches of independent
+ *    images (the reference handles one 2-D image per call; n = 1 is that).
+ *  - "_dev" pointers are CUDA device pointers owned by the caller; nothing is
+ *    retained after return.  "_host" entry points take host pointers and do
+ *    the host<->device copies inside the call.
+ *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is stream-ordered and returns after the stream has drained
+ *    the call's work (errors are device-checked before returning).
+ *  - fg: foreground adjacency, 8 -> the (8,4) pair (ADJ_84), 4 -> (4,8)
+ *    (ADJ_48), grid.py:22-45.
+ *  - Return value: TS_OK or an error class; ts_last_error() gives the
+ *    message (thread-local).  TS_ERR_VALUE corresponds to the reference's
+ *    ValueError conditions (same messages).
+ */
+#ifndef TOPOSMOOTH_B200_H
+#define TOPOSMOOTH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_OK 0
+#define TS_ERR_VALUE 1        /* invalid argument / input (reference ValueError) */
+#define TS_ERR_CUDA 2         /* CUDA runtime failure */
+#define TS_ERR_INTERNAL 3     /* device-side invariant violated (never silently truncates) */
+#define TS_ERR_UNSUPPORTED 4  /* outside the device path's limits (e.g. r > 16) */
+
+/* Library version, e.g. 100 for 0.1.0. */
+int ts_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *ts_last_error(void);
+
+/* Largest radius the fused HASF kernel is instantiated for (16). */
+int ts_max_radius(void);
+
+/* HASF: alternate homotopic cutting and filling at radii 1..r_max.
+ * Replaces hasf(img, SmoothingConfig(r_max, adj, keep, avoid)) and smooth(img, r_max)
+ * (smoothing.py:187-217).  keep_dev / avoid_dev: [n][h][w] constraint images or
+ * NULL.  stats_host: NULL or int64[n*4] receiving per image (sweeps, fixpoint
+ * passes, engine calls, flips). */
+int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
+                  int32_t r_max, int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev,
+                  void *stream, int64_t *stats_host);
+
+/* Same, from host buffers (copies in/out inside the call; pinned buffers are
+ * copied asynchronously, pageable ones are staged by the CUDA runtime). */
+int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w,
+                       int32_t r_max, int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host,
+                       void *stream);
+
+/* One homotopic cutting at radius r (smoothing.py:127-135, 149-165). keep_dev may be NULL. */
+int ts_cutting_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
+                     int32_t r, int32_t fg, const uint8_t *keep_dev, void *stream);
+
+/* One homotopic filling at radius r (smoothing.py:138-146, 168-184). avoid_dev may be NULL. */
+int ts_filling_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
+                     int32_t r, int32_t fg, const uint8_t *avoid_dev, void *stream);
+
+/* Priority-ordered homotopic thinning (topo.py:279-314): removes simple object
+ * points outside keep in (priority, raster) order; max_iter < 0 = unbounded. */
+int ts_thin_batch(const uint8_t *img_dev, const uint8_t *keep_dev, const int64_t *prio_dev,
+                  uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t fg, int64_t max_iter,
+                  void *stream);
+
+/* Priority-ordered homotopic thickening inside allowed (topo.py:317-354). */
+int ts_thicken_batch(const uint8_t *img_dev, const uint8_t *allowed_dev, const int64_t *prio_dev,
+                     uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t fg, int64_t max_iter,
+                     void *stream);
+
+/* Exact squared EDT, int64 out, INF = h^2 + w^2 + 1 where no seed.
+ * mode 0: distance to object pixels (edt_squared, edt.py:173-187);
+ * mode 1: distance to background incl. the window exterior
+ *         (background_distances, morph.py:34-42). */
+int ts_edt_sq_batch(const uint8_t *in_dev, int64_t *out_dev, int64_t n, int32_t h, int32_t w,
+                    int32_t mode, void *stream);
+
+/* Phase 1 alone: vertical distances G (edt_phase1_columns, edt.py:122-136). */
+int ts_edt_phase1_batch(const uint8_t *in_dev, int64_t *g_dev, int64_t n, int32_t h, int32_t w,
+                        void *stream);
+
+/* Phase 2 alone: row lower envelopes from G (edt_phase2_rows, edt.py:139-149). */
+int ts_edt_phase2_batch(const int64_t *g_dev, int64_t *out_dev, int64_t n, int32_t h, int32_t w,
+                        void *stream);
+
+/* Ball dilation / erosion by EDT thresholding (dilate / erode, morph.py:45-59). */
+int ts_dilate_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
+                    int32_t r, void *stream);
+int ts_erode_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
+                   int32_t r, void *stream);
+
+/* 8-bit neighbour codes (neighborhood_codes, topo.py:97-106). */
+int ts_neighborhood_codes_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
+                                int32_t w, void *stream);
+
+/* Simple object points, LUT staged in shared memory (simple_point_mask, topo.py:144-148). */
+int ts_simple_point_mask_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
+                               int32_t w, int32_t fg, void *stream);
+
+/* Host tables: component counts T8/T4 of every 8-bit code and the simple-point
+ * LUTs (T8_TABLE, T4_TABLE, SIMPLE_84, SIMPLE_48, topo.py:79-84). */
+int ts_connectivity_tables(uint8_t *t8_256, uint8_t *t4_256, uint8_t *s84_256, uint8_t *s48_256);
+
+/* Evaluates the engine's bit-sliced simple-point circuit on all 256 codes on
+ * the device (must equal SIMPLE_84 / SIMPLE_48). */
+int ts_selftest_circuit(uint8_t *s84_256_host, uint8_t *s48_256_host);
+
+/* Tuning: shared-memory budget (bytes) for the fused kernel's per-image
+ * buffers; 0 = device maximum.  Returns the previous value. */
+int64_t ts_set_smem_budget(int64_t bytes);
+
+/* Placement/occupancy the fused kernel would use for an image shape:
+ * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
+ * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA. */
+int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid,
+                 int64_t *info5);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOPOSMOOTH_B200_H */

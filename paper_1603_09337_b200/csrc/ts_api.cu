@@ -1,0 +1,482 @@
+// C ABI of the B200 HASF path (see include/toposmooth_b200.h).
+//
+// Host-side responsibilities: argument checks, per-call workspace planning
+// (which per-image buffers of the fused kernel live in shared memory and
+// which in the CTA's slice of an L2-resident global workspace), launches on
+// the caller's stream, and surfacing device-side error flags as status codes
+// (nothing is ever returned silently wrong).  No global mutable state besides
+// the thread-local error string and the shared-memory budget knob.
+#include <cuda_runtime.h>
+#include <atomic>
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/toposmooth_b200.h"
+#include "ts_common.cuh"
+#include "ts_internal.h"
+
+namespace ts {
+cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream);
+cudaError_t hasf_occupancy(int fg, size_t smem_bytes, int *blocks_per_sm);
+int hasf_threads();
+cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
+                              cudaStream_t st);
+cudaError_t launch_edt_phase2(const long long *g, void *out, long long *stk, int n, int H, int W, long long inf,
+                              int out_mode, long long thr, cudaStream_t st);
+cudaError_t launch_classify(const uint8_t *pix, uint8_t *out, int n, int H, int W, const uint8_t *lut,
+                            cudaStream_t st);
+cudaError_t launch_selftest_circuit(uint8_t *out84, uint8_t *out48, cudaStream_t st);
+}  // namespace ts
+
+using namespace ts;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_smem_budget{0};
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+int ok() {
+    g_err.clear();
+    return TS_OK;
+}
+int cuda_fail(cudaError_t e, const char *where) {
+    return fail(TS_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TS_CUDA(call)                                   \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// ---- connectivity tables, restated from their definition -----------------
+// T_conn(code) = number of conn-components of the set neighbours of the 3x3
+// window's centre that are conn-adjacent to the centre (topo.py:44-84).
+const int kOffR[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+const int kOffC[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+
+int comp_count(int mask, int conn) {
+    int parent[8];
+    for (int i = 0; i < 8; ++i) parent[i] = i;
+    auto find = [&](int a) {
+        while (parent[a] != a) a = parent[a] = parent[parent[a]];
+        return a;
+    };
+    auto adjacent = [&](int a, int b) {
+        int dr = kOffR[a] - kOffR[b], dc = kOffC[a] - kOffC[b];
+        dr = dr < 0 ? -dr : dr;
+        dc = dc < 0 ? -dc : dc;
+        return conn == 4 ? (dr + dc == 1) : (dr <= 1 && dc <= 1 && (dr | dc));
+    };
+    for (int a = 0; a < 8; ++a)
+        for (int b = a + 1; b < 8; ++b)
+            if (((mask >> a) & 1) && ((mask >> b) & 1) && adjacent(a, b)) parent[find(a)] = find(b);
+    int roots = 0;   // bitmask of component roots touching the centre
+    for (int a = 0; a < 8; ++a) {
+        if (!((mask >> a) & 1)) continue;
+        const bool touches = conn == 8 || (kOffR[a] == 0 || kOffC[a] == 0);
+        if (touches) roots |= 1 << find(a);
+    }
+    return __builtin_popcount(roots);
+}
+
+struct Tables {
+    uint8_t t8[256], t4[256], s84[256], s48[256];
+    Tables() {
+        for (int m = 0; m < 256; ++m) {
+            t8[m] = (uint8_t)comp_count(m, 8);
+            t4[m] = (uint8_t)comp_count(m, 4);
+        }
+        for (int m = 0; m < 256; ++m) {
+            s84[m] = (t8[m] == 1 && t4[m ^ 0xFF] == 1);
+            s48[m] = (t4[m] == 1 && t8[m ^ 0xFF] == 1);
+        }
+    }
+};
+const Tables &tables() {
+    static const Tables t;
+    return t;
+}
+
+// ---- fused-kernel planning ------------------------------------------------
+struct Plan {
+    int WW = 0, nwords = 0, slices = 0;
+    int per_sm = 0, per_wave = 0;
+    size_t smem_bytes = 0;
+    uint32_t mask = 0;
+    long long off[B_COUNT] = {};
+    long long stride = 0;   // global words per CTA
+};
+
+int device_props(int *sms, int *smem_optin) {
+    int dev = 0;
+    TS_CUDA(cudaGetDevice(&dev));
+    TS_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+    TS_CUDA(cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    return TS_OK;
+}
+
+int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl) {
+    pl.WW = (W + 31) / 32;
+    const long long nw = (long long)H * pl.WW;
+    if (H >= 65536 || pl.WW >= 65536 || nw * 8 >= (long long)INT_MAX)
+        return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel (h < 65536, w < 2^21, h*w/32*8 < 2^31)");
+    pl.nwords = (int)nw;
+    pl.slices = (mode == MODE_HASF && r_last >= 1) ? rank_slices(r_last) : 0;
+    auto r4 = [](long long x) { return (x + 3) & ~3LL; };
+    long long size[B_COUNT];
+    size[B_I] = r4(nw);
+    size[B_D] = r4(nw);
+    size[B_C] = r4(nw);
+    size[B_DIRTY] = r4(((nw + 15) / 16) * 4);
+    size[B_LIST] = r4(nw);
+    size[B_E] = r4(8 * nw);
+    size[B_B] = r4(nw);
+    size[B_XS] = mode == MODE_HASF ? r4(nw) : 0;
+    size[B_R] = r4((long long)pl.slices * nw);
+    size[B_K] = (mode == MODE_HASF && has_k) ? r4(nw) : 0;
+    size[B_A] = (mode == MODE_HASF && has_a) ? r4(nw) : 0;
+
+    int sms = 0, optin = 0;
+    int rc = device_props(&sms, &optin);
+    if (rc) return rc;
+    long long budget = optin - 256;   // static shared scalars of the kernel
+    const long long knob = g_smem_budget.load();
+    if (knob > 0 && knob < budget) budget = knob;
+    long long used = 0, gused = 0;
+    pl.mask = 0;
+    for (int b = 0; b < B_COUNT; ++b) {
+        if (size[b] == 0) {
+            pl.off[b] = 0;
+            continue;
+        }
+        if ((used + size[b]) * 4 <= budget) {
+            pl.mask |= 1u << b;
+            pl.off[b] = used;
+            used += size[b];
+        } else {
+            pl.off[b] = gused;
+            gused += size[b];
+        }
+    }
+    pl.smem_bytes = (size_t)(used * 4);
+    pl.stride = gused;
+    int per_sm = 0;
+    TS_CUDA(hasf_occupancy(fg, pl.smem_bytes, &per_sm));
+    if (per_sm < 1) return fail(TS_ERR_CUDA, "fused kernel does not fit on an SM");
+    pl.per_sm = per_sm;
+    pl.per_wave = per_sm * sms;
+    return TS_OK;
+}
+
+const char *err_message(int code, int mode) {
+    switch (code) {
+        case ERR_NOT_BINARY:
+        case ERR_CONSTRAINT_NOT_BINARY:
+            return "binary image pixels must be 0 or 1";                               // grid.py:60-61
+        case ERR_KEEP_NOT_OBJECT:
+            return mode == MODE_THIN ? "constraint pixels must be a subset of the object pixels"   // topo.py:265
+                                     : "keep-constraint pixels must be object pixels";              // smoothing.py:204
+        case ERR_AVOID_ON_OBJECT:
+            return "avoid-constraint pixels must be background pixels";                 // smoothing.py:206
+        case ERR_KEEP_AVOID:
+            return "keep and avoid constraints overlap";                                // smoothing.py:202
+        case ERR_ALLOWED_NOT_SUPERSET:
+            return "object pixels must be a subset of the allowed set";                 // topo.py:333
+        case ERR_JACOBI_CAP:
+            return "internal: fixpoint iteration exceeded its bound";
+        case ERR_SWEEP_CAP:
+            return "internal: engine exceeded its sweep bound";
+        default:
+            return "internal: unknown device error";
+    }
+}
+
+int check_shape(int64_t n, int32_t h, int32_t w) {
+    if (n < 0) return fail(TS_ERR_VALUE, "batch size must be >= 0");
+    if (h < 1 || w < 1)
+        return fail(TS_ERR_VALUE, "expected a 2D image with positive dimensions, got shape (" + std::to_string(h) +
+                                      ", " + std::to_string(w) + ")");
+    if (n > INT_MAX) return fail(TS_ERR_UNSUPPORTED, "batch too large");
+    return TS_OK;
+}
+
+int check_fg(int32_t fg) {
+    if (fg != 8 && fg != 4) return fail(TS_ERR_VALUE, "foreground adjacency must be 4 or 8, got " + std::to_string(fg));
+    return TS_OK;
+}
+
+// runs the fused kernel over a batch; waits for completion and checks the
+// device error flag
+int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last,
+              int do_cut, int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, const int64_t *prio,
+              long long max_sweeps, cudaStream_t st, int64_t *stats_host) {
+    int rc;
+    if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
+    if (r_last > kMaxR)
+        return fail(TS_ERR_UNSUPPORTED, "radius " + std::to_string(r_last) + " exceeds the device path's maximum " +
+                                            std::to_string(kMaxR));
+    if (n == 0) return ok();
+    Plan pl;
+    if ((rc = make_plan(h, w, r_last, mode, keep != nullptr, avoid != nullptr, fg, pl))) return rc;
+    const int grid = (int)std::min<long long>(n, pl.per_wave);
+    const size_t ws_words = (size_t)pl.stride * grid;
+    const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * 4 * sizeof(long long) : 0);
+    char *ctrl = nullptr;
+    uint32_t *gws = nullptr;
+    TS_CUDA(cudaMallocAsync((void **)&ctrl, ctrl_bytes, st));
+    if (ws_words) {
+        cudaError_t e = cudaMallocAsync((void **)&gws, ws_words * 4, st);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(ctrl, st);
+            return cuda_fail(e, "cudaMallocAsync(workspace)");
+        }
+    }
+    TS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, st));
+    KParams p{};
+    p.in = in;
+    p.out = out;
+    p.keep = keep;
+    p.avoid = avoid;
+    p.prio = prio;
+    p.n = (int)n;
+    p.H = h;
+    p.W = w;
+    p.WW = pl.WW;
+    p.nwords = pl.nwords;
+    p.r_first = r_first;
+    p.r_last = r_last;
+    p.do_cut = do_cut;
+    p.do_fill = do_fill;
+    p.mode = mode;
+    p.max_sweeps = max_sweeps;
+    p.slices = pl.slices;
+    p.gws = gws;
+    p.gws_stride = pl.stride;
+    p.smem_mask = pl.mask;
+    for (int b = 0; b < B_COUNT; ++b) p.off[b] = pl.off[b];
+    p.counter = reinterpret_cast<int *>(ctrl);
+    p.err = reinterpret_cast<int *>(ctrl + 16);
+    p.stats = stats_host ? reinterpret_cast<long long *>(ctrl + 64) : nullptr;
+    cudaError_t le = launch_hasf(p, fg, grid, pl.smem_bytes, st);
+    int herr = 0;
+    cudaError_t ce = cudaSuccess;
+    if (le == cudaSuccess) ce = cudaMemcpyAsync(&herr, ctrl + 16, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (le == cudaSuccess && ce == cudaSuccess && stats_host)
+        ce = cudaMemcpyAsync(stats_host, ctrl + 64, (size_t)n * 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    if (gws) cudaFreeAsync(gws, st);
+    cudaFreeAsync(ctrl, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (le != cudaSuccess) return cuda_fail(le, "launch hasf_kernel");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
+    if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
+    if (herr) {
+        const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP;
+        return fail(internal ? TS_ERR_INTERNAL : TS_ERR_VALUE, err_message(herr, mode));
+    }
+    return ok();
+}
+
+}  // namespace
+
+extern "C" {
+
+int ts_version(void) { return 100; }
+
+const char *ts_last_error(void) { return g_err.c_str(); }
+
+int ts_max_radius(void) { return kMaxR; }
+
+int64_t ts_set_smem_budget(int64_t bytes) { return g_smem_budget.exchange(bytes < 0 ? 0 : bytes); }
+
+int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {
+    int rc;
+    if ((rc = check_shape(1, h, w))) return rc;
+    Plan pl;
+    if ((rc = make_plan(h, w, r_max, MODE_HASF, has_keep != 0, has_avoid != 0, 8, pl))) return rc;
+    info5[0] = pl.per_wave;
+    info5[1] = pl.per_sm;
+    info5[2] = (int64_t)pl.smem_bytes;
+    info5[3] = pl.mask;
+    info5[4] = pl.stride * 4;
+    return ok();
+}
+
+int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                  int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev, void *stream,
+                  int64_t *stats_host) {
+    if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
+    return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr, -1,
+                     (cudaStream_t)stream, stats_host);
+}
+
+int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                       int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host, void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w))) return rc;
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = (size_t)n * h * w;
+    uint8_t *d = nullptr;
+    const int nbuf = 2 + (keep_host ? 1 : 0) + (avoid_host ? 1 : 0);
+    TS_CUDA(cudaMallocAsync((void **)&d, bytes * nbuf, st));
+    uint8_t *din = d, *dout = d + bytes;
+    uint8_t *dk = keep_host ? d + 2 * bytes : nullptr;
+    uint8_t *da = avoid_host ? d + (2 + (keep_host ? 1 : 0)) * bytes : nullptr;
+    cudaError_t e = cudaMemcpyAsync(din, in_host, bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && dk) e = cudaMemcpyAsync(dk, keep_host, bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && da) e = cudaMemcpyAsync(da, avoid_host, bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(d, st);
+        return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    }
+    rc = ts_hasf_batch(din, dout, n, h, w, r_max, fg, dk, da, stream, nullptr);
+    if (rc == TS_OK) {
+        e = cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(D2H)");
+    }
+    const std::string keep_msg = g_err;
+    cudaFreeAsync(d, st);
+    cudaStreamSynchronize(st);
+    g_err = keep_msg;
+    return rc;
+}
+
+int ts_cutting_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r, int32_t fg,
+                     const uint8_t *keep_dev, void *stream) {
+    if (r < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
+    return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, r == 0 ? 1 : r, r, 1, 0, fg, keep_dev, nullptr, nullptr,
+                     -1, (cudaStream_t)stream, nullptr);
+}
+
+int ts_filling_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r, int32_t fg,
+                     const uint8_t *avoid_dev, void *stream) {
+    if (r < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
+    return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, r == 0 ? 1 : r, r, 0, 1, fg, nullptr, avoid_dev, nullptr,
+                     -1, (cudaStream_t)stream, nullptr);
+}
+
+int ts_thin_batch(const uint8_t *img_dev, const uint8_t *keep_dev, const int64_t *prio_dev, uint8_t *out_dev,
+                  int64_t n, int32_t h, int32_t w, int32_t fg, int64_t max_iter, void *stream) {
+    if (!keep_dev || !prio_dev) return fail(TS_ERR_VALUE, "keep and priority are required");
+    return run_fused(MODE_THIN, img_dev, out_dev, n, h, w, 1, 0, 0, 0, fg, keep_dev, nullptr, prio_dev,
+                     max_iter < 0 ? -1 : max_iter, (cudaStream_t)stream, nullptr);
+}
+
+int ts_thicken_batch(const uint8_t *img_dev, const uint8_t *allowed_dev, const int64_t *prio_dev, uint8_t *out_dev,
+                     int64_t n, int32_t h, int32_t w, int32_t fg, int64_t max_iter, void *stream) {
+    if (!allowed_dev || !prio_dev) return fail(TS_ERR_VALUE, "allowed and priority are required");
+    return run_fused(MODE_THICKEN, img_dev, out_dev, n, h, w, 1, 0, 0, 0, fg, allowed_dev, nullptr, prio_dev,
+                     max_iter < 0 ? -1 : max_iter, (cudaStream_t)stream, nullptr);
+}
+
+static int run_edt(const uint8_t *in, const int64_t *g_in, void *out, int64_t n, int32_t h, int32_t w, int invert,
+                   int out_mode, long long thr, bool phase1_only, cudaStream_t st) {
+    int rc;
+    if ((rc = check_shape(n, h, w))) return rc;
+    if (h > 32767 || w > 32767) return fail(TS_ERR_UNSUPPORTED, "exact EDT supports h, w <= 32767");
+    if (n == 0) return ok();
+    const long long inf = (long long)h * h + (long long)w * w + 1;   // edt.py:25-28
+    const size_t px = (size_t)n * h * w;
+    long long *g = nullptr, *stk = nullptr;
+    if (phase1_only) {
+        TS_CUDA(launch_edt_phase1(in, reinterpret_cast<long long *>(out), (int)n, h, w, invert, inf, st));
+        TS_CUDA(cudaStreamSynchronize(st));
+        return ok();
+    }
+    TS_CUDA(cudaMallocAsync((void **)&stk, sizeof(long long) * (px * 2 + (g_in ? 0 : px)), st));
+    g = g_in ? const_cast<long long *>(reinterpret_cast<const long long *>(g_in)) : stk + 2 * px;
+    cudaError_t e = cudaSuccess;
+    if (!g_in) e = launch_edt_phase1(in, g, (int)n, h, w, invert, inf, st);
+    if (e == cudaSuccess) e = launch_edt_phase2(g, out, stk, (int)n, h, w, inf, out_mode, thr, st);
+    cudaFreeAsync(stk, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "edt launch");
+    if (se != cudaSuccess) return cuda_fail(se, "edt kernels");
+    return ok();
+}
+
+int ts_edt_sq_batch(const uint8_t *in_dev, int64_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t mode,
+                    void *stream) {
+    if (mode != 0 && mode != 1) return fail(TS_ERR_VALUE, "mode must be 0 (object) or 1 (background)");
+    return run_edt(in_dev, nullptr, out_dev, n, h, w, mode, mode, 0, false, (cudaStream_t)stream);
+}
+
+int ts_edt_phase1_batch(const uint8_t *in_dev, int64_t *g_dev, int64_t n, int32_t h, int32_t w, void *stream) {
+    return run_edt(in_dev, nullptr, g_dev, n, h, w, 0, 0, 0, true, (cudaStream_t)stream);
+}
+
+int ts_edt_phase2_batch(const int64_t *g_dev, int64_t *out_dev, int64_t n, int32_t h, int32_t w, void *stream) {
+    return run_edt(nullptr, g_dev, out_dev, n, h, w, 0, 0, 0, false, (cudaStream_t)stream);
+}
+
+int ts_dilate_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r,
+                    void *stream) {
+    if (r < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
+    return run_edt(in_dev, nullptr, out_dev, n, h, w, 0, 2, (long long)r * r, false, (cudaStream_t)stream);
+}
+
+int ts_erode_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r,
+                   void *stream) {
+    if (r < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
+    return run_edt(in_dev, nullptr, out_dev, n, h, w, 1, 3, (long long)r * r, false, (cudaStream_t)stream);
+}
+
+int ts_neighborhood_codes_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
+                                void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w))) return rc;
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    TS_CUDA(launch_classify(in_dev, out_dev, (int)n, h, w, nullptr, st));
+    TS_CUDA(cudaStreamSynchronize(st));
+    return ok();
+}
+
+int ts_simple_point_mask_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t fg,
+                               void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *dlut = nullptr;
+    TS_CUDA(cudaMallocAsync((void **)&dlut, 256, st));
+    const uint8_t *src = fg == 8 ? tables().s84 : tables().s48;
+    cudaError_t e = cudaMemcpyAsync(dlut, src, 256, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = launch_classify(in_dev, out_dev, (int)n, h, w, dlut, st);
+    cudaFreeAsync(dlut, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "simple_point_mask");
+    if (se != cudaSuccess) return cuda_fail(se, "simple_point_mask");
+    return ok();
+}
+
+int ts_connectivity_tables(uint8_t *t8, uint8_t *t4, uint8_t *s84, uint8_t *s48) {
+    const Tables &t = tables();
+    if (t8) std::memcpy(t8, t.t8, 256);
+    if (t4) std::memcpy(t4, t.t4, 256);
+    if (s84) std::memcpy(s84, t.s84, 256);
+    if (s48) std::memcpy(s48, t.s48, 256);
+    return ok();
+}
+
+int ts_selftest_circuit(uint8_t *s84, uint8_t *s48) {
+    uint8_t *d = nullptr;
+    TS_CUDA(cudaMalloc((void **)&d, 512));
+    cudaError_t e = launch_selftest_circuit(d, d + 256, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(s84, d, 256, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(s48, d + 256, 256, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "selftest_circuit");
+    return ok();
+}
+
+}  // extern "C"

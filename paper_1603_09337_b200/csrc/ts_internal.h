@@ -1,0 +1,59 @@
+// Host/device shared parameter blocks (internal; not part of the C ABI).
+#pragma once
+#include <cstdint>
+
+namespace ts {
+
+// Per-image working buffers of the fused HASF kernel.  Each lives either in
+// the CTA's shared memory or in its private slice of a global workspace
+// (L2-resident); the host places them greedily in this priority order.
+enum Buf : int {
+    B_I = 0,     // current image, bit-packed                          nwords
+    B_D,         // Jacobi decisions of the current sweep              nwords
+    B_C,         // candidates of the current sweep                    nwords
+    B_DIRTY,     // per-word "re-examine" flags (bytes)                ceil16(nwords)/4
+    B_LIST,      // active-word list, (y << 16) | x                    nwords
+    B_E,         // 8 "earlier neighbour" masks per word, interleaved  8 * nwords
+    B_B,         // blocked (floor) plane                              nwords
+    B_XS,        // saved image (cutting input X / filling input X')   nwords
+    B_R,         // rank bit-slices of the clamped distance map        S * nwords
+    B_K,         // keep constraint plane (optional)                   nwords
+    B_A,         // avoid constraint plane (optional)                  nwords
+    B_COUNT
+};
+
+enum Mode : int { MODE_HASF = 0, MODE_THIN = 1, MODE_THICKEN = 2 };
+
+enum Err : int {
+    ERR_NONE = 0,
+    ERR_NOT_BINARY = 1,        // input pixel not in {0,1}
+    ERR_JACOBI_CAP = 2,        // fixpoint iteration exceeded its proven bound
+    ERR_SWEEP_CAP = 3,         // engine exceeded its proven sweep bound
+    ERR_KEEP_NOT_OBJECT = 4,   // keep constraint outside the object
+    ERR_AVOID_ON_OBJECT = 5,   // avoid constraint on object pixels
+    ERR_KEEP_AVOID = 6,        // keep and avoid overlap
+    ERR_CONSTRAINT_NOT_BINARY = 7,
+    ERR_ALLOWED_NOT_SUPERSET = 8,  // thicken: object outside allowed
+};
+
+struct KParams {
+    const uint8_t *in;
+    uint8_t *out;
+    const uint8_t *keep;    // [n,h,w] or null  (MODE_THIN: keep; MODE_THICKEN: allowed)
+    const uint8_t *avoid;   // [n,h,w] or null
+    const int64_t *prio;    // [n,h,w] (engine modes only)
+    int n, H, W, WW, nwords;
+    int r_first, r_last, do_cut, do_fill;
+    int mode;
+    long long max_sweeps;   // < 0: unbounded
+    int slices;             // rank slices allocated (for r_last)
+    uint32_t *gws;          // global workspace, gws_stride words per CTA
+    long long gws_stride;
+    uint32_t smem_mask;     // bit b set: buffer b lives in shared memory
+    long long off[B_COUNT]; // word offset of each buffer (smem or CTA slice)
+    int *counter;           // image queue head
+    int *err;               // first error code (atomicCAS from 0)
+    long long *stats;       // [n][4]: sweeps, jacobi passes, engine calls, flips (or null)
+};
+
+}  // namespace ts

@@ -1,0 +1,202 @@
+"""Parity of the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Bit-exact everywhere (all arithmetic is integer)."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1603_09337_b200 as P
+from paper_1603_09337_b200 import _lib
+from paper_1603_09337_b200 import workloads as W
+from conftest import golden_cases, random_image
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def test_circuit_equals_lut_on_device():
+    import ctypes
+    a, b = (ctypes.c_uint8 * 256)(), (ctypes.c_uint8 * 256)()
+    _lib.check(_lib.load().ts_selftest_circuit(ctypes.addressof(a), ctypes.addressof(b)))
+    assert np.array_equal(np.frombuffer(a, np.uint8), P.SIMPLE_84)
+    assert np.array_equal(np.frombuffer(b, np.uint8), P.SIMPLE_48)
+
+
+def test_edt_golden():
+    for c in golden_cases("edt"):
+        assert np.array_equal(P.edt_squared(c["img"]), c["out"]), c["name"]
+
+
+def test_edt_phases():
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        img = random_image(rng, int(rng.integers(1, 40)), int(rng.integers(1, 40)), rng.uniform(0.05, 0.9))
+        g = P.edt_phase1_columns(img)
+        assert np.array_equal(g, O.edt_phase1_columns(img))
+        assert np.array_equal(P.edt_phase2_rows(g), O.edt_phase2_rows(g))
+    img = np.zeros((3, 3), np.uint8)
+    img[0, 0] = 1
+    assert P.edt_phase2_rows(P.edt_phase1_columns(img))[2, 2] == 8
+
+
+def test_edt_large_vs_oracle():
+    for cfg in ("c1", "c4"):
+        img = W.config_image(cfg, 3)
+        assert np.array_equal(P.edt_squared(img), O.edt_squared(img))
+        assert np.array_equal(P.background_distances(img), O.background_distances(img))
+
+
+def test_morph_golden():
+    for c in golden_cases("morph"):
+        assert np.array_equal(P.background_distances(c["img"]), c["bgd"]), c["name"]
+        assert np.array_equal(P.dilate(c["img"], c["r"]), c["dil"]), c["name"]
+        assert np.array_equal(P.erode(c["img"], c["r"]), c["ero"]), c["name"]
+
+
+def test_codes_and_simple_mask():
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        img = random_image(rng, int(rng.integers(1, 50)), int(rng.integers(1, 50)), rng.uniform(0.1, 0.9))
+        assert np.array_equal(P.neighborhood_codes(img), O.neighborhood_codes(img))
+        for adj in (P.ADJ_84, P.ADJ_48):
+            assert np.array_equal(P.simple_point_mask(img, adj), O.simple_point_mask(img, adj.fg))
+
+
+def test_engine_golden():
+    for c in golden_cases("engine"):
+        adj = P.ADJ_84 if c["fg"] == 8 else P.ADJ_48
+        mi = None if c["max_iter"] < 0 else c["max_iter"]
+        assert np.array_equal(P.homotopic_thin(c["img"], c["keep"], c["pri"], adj, max_iter=mi), c["thin"]), c["name"]
+        got = P.homotopic_thicken(c["img"], c["allowed"], c["pri"], adj, max_iter=mi)
+        assert np.array_equal(got, c["thick"]), c["name"]
+
+
+def test_engine_random_vs_oracle():
+    rng = np.random.default_rng(12)
+    for i in range(60):
+        h, w = int(rng.integers(1, 80)), int(rng.integers(1, 80))
+        fg = 8 if i % 2 else 4
+        adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+        img = random_image(rng, h, w, rng.uniform(0.2, 0.9))
+        keep = (img & random_image(rng, h, w, 0.05)).astype(np.uint8)
+        pri = rng.integers(0, [3, 10, 1000][i % 3], (h, w)).astype(np.int64)
+        mi = [None, 1, 3][i % 3]
+        assert np.array_equal(P.homotopic_thin(img, keep, pri, adj, max_iter=mi),
+                              O.homotopic_thin(img, keep, pri, fg, mi)), i
+        allowed = (img | random_image(rng, h, w, 0.5)).astype(np.uint8)
+        assert np.array_equal(P.homotopic_thicken(img, allowed, pri, adj, max_iter=mi),
+                              O.homotopic_thicken(img, allowed, pri, fg, mi)), i
+
+
+def test_halves_golden():
+    for c in golden_cases("halves"):
+        adj = P.ADJ_84 if c["fg"] == 8 else P.ADJ_48
+        assert np.array_equal(P.homotopic_cutting(c["img"], c["keep"], c["r"], adj), c["cut"]), c["name"]
+        assert np.array_equal(P.homotopic_filling(c["img"], c["avoid"], c["r"], adj), c["fill"]), c["name"]
+
+
+def test_hasf_small_golden():
+    for c in golden_cases("hasf_small"):
+        adj = P.ADJ_84 if c["fg"] == 8 else P.ADJ_48
+        keep = c["keep"] if c["keep"].any() else None
+        avoid = c["avoid"] if c["avoid"].any() else None
+        out = P.hasf(c["img"], P.SmoothingConfig(r_max=c["r"], adj=adj, keep=keep, avoid=avoid))
+        assert np.array_equal(out, c["out"]), c["name"]
+
+
+@pytest.mark.parametrize("name", ["c0_0", "c1_0", "c1_1", "c1_2", "c1_3", "c4_0", "c4_1", "c4_2", "c4_3", "c4_4",
+                                  "c4_5", "c4_6", "c4_7", "jagged_disc_r5", "noisy_disc_r5", "c2_0"])
+def test_hasf_config_golden(name):
+    c = next(x for x in golden_cases("hasf_configs") if x["name"] == name)
+    adj = P.ADJ_84 if c["fg"] == 8 else P.ADJ_48
+    out = P.hasf(c["img"], P.SmoothingConfig(r_max=c["r"], adj=adj))
+    assert np.array_equal(out, c["out"])
+
+
+def test_hasf_batch_matches_single_and_golden():
+    cases = [x for x in golden_cases("hasf_configs") if x["name"].startswith("c4_")]
+    imgs = np.stack([c["img"] for c in cases])
+    out = P.hasf_batch(torch.from_numpy(imgs).cuda(), 4, P.ADJ_48)
+    assert out.is_cuda and out.dtype == torch.uint8
+    for k, c in enumerate(cases):
+        assert np.array_equal(out[k].cpu().numpy(), c["out"]), c["name"]
+    host = P.hasf_batch_host(imgs, 4, P.ADJ_48)
+    assert np.array_equal(host, out.cpu().numpy())
+
+
+def test_hasf_batch_ragged_shapes_vs_oracle():
+    rng = np.random.default_rng(13)
+    for (h, w) in [(1, 1), (1, 77), (77, 1), (2, 2), (33, 31), (31, 33), (64, 96), (5, 200), (130, 65)]:
+        imgs = np.stack([random_image(rng, h, w, rng.uniform(0.2, 0.8)) for _ in range(5)])
+        for fg in (8, 4):
+            adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+            got = P.hasf_batch(imgs, 3, adj)
+            want = O.hasf_batch(imgs, 3, fg, threads=4)
+            assert np.array_equal(got, want), (h, w, fg)
+
+
+def test_hasf_batch_constraints_vs_oracle():
+    rng = np.random.default_rng(14)
+    imgs = np.stack([random_image(rng, 48, 70, 0.5) for _ in range(6)])
+    keep = (imgs & (rng.random(imgs.shape) < 0.05)).astype(np.uint8)
+    avoid = (((rng.random(imgs.shape) < 0.05)) & (imgs == 0)).astype(np.uint8)
+    got = P.hasf_batch(imgs, 4, P.ADJ_84, keep=keep, avoid=avoid)
+    want = O.hasf_batch(imgs, 4, 8, keep=keep, avoid=avoid, threads=4)
+    assert np.array_equal(got, want)
+
+
+def test_degenerate_images():
+    for img in (np.zeros((64, 64), np.uint8), np.ones((64, 64), np.uint8), np.zeros((1, 1), np.uint8),
+                np.ones((1, 1), np.uint8), np.ones((1, 40), np.uint8)):
+        for r in (0, 1, 3):
+            assert np.array_equal(P.smooth(img, r), O.hasf(img, r, 8))
+    assert P.hasf_batch(np.zeros((0, 8, 8), np.uint8), 2).shape == (0, 8, 8)
+
+
+def test_device_validation_errors():
+    bad = np.zeros((2, 8, 8), np.uint8)
+    bad[1, 3, 3] = 2
+    with pytest.raises(ValueError, match="binary image pixels"):
+        P.hasf_batch(torch.from_numpy(bad).cuda(), 1)
+    imgs = np.zeros((2, 8, 8), np.uint8)
+    keep = np.zeros_like(imgs)
+    keep[0, 1, 1] = 1
+    with pytest.raises(ValueError, match="keep-constraint"):
+        P.hasf_batch(imgs, 1, keep=keep)
+    imgs[1, 2, 2] = 1
+    avoid = np.zeros_like(imgs)
+    avoid[1, 2, 2] = 1
+    with pytest.raises(ValueError, match="avoid-constraint"):
+        P.hasf_batch(imgs, 1, avoid=avoid)
+    with pytest.raises(RuntimeError, match="exceeds"):
+        P.smooth(np.zeros((8, 8), np.uint8), 17)
+
+
+def test_topology_invariants_full_size_batches():
+    """c1 / c4 shaped batches: component counts of X (fg-adjacency) and of the
+    background with the window exterior attached (bg-adjacency) are preserved."""
+    for cfg_name, count in (("c1", 8), ("c4", 32)):
+        cfg = W.CONFIGS[cfg_name]
+        imgs = W.config_batch(cfg, 100, count)
+        out = P.hasf_batch(imgs, cfg.r_max, P.ADJ_84 if cfg.fg == 8 else P.ADJ_48)
+        for a, b in zip(imgs, out):
+            assert O.topology_preserved(a, b, cfg.fg)
+
+
+def test_hasf_batch_vs_oracle_c1_c4_samples():
+    for cfg_name, start, count in (("c1", 200, 3), ("c4", 500, 16)):
+        cfg = W.CONFIGS[cfg_name]
+        imgs = W.config_batch(cfg, start, count)
+        got = P.hasf_batch(imgs, cfg.r_max, P.ADJ_84 if cfg.fg == 8 else P.ADJ_48)
+        want = O.hasf_batch(imgs, cfg.r_max, cfg.fg)
+        assert np.array_equal(got, want), cfg_name
+
+
+def test_stats_are_reported():
+    imgs = W.config_batch("c0", 0, 1)
+    out, st = P.hasf_batch(imgs, 3, stats=True)
+    assert st.shape == (1, 4)
+    assert st[0, 2] == 12 and st[0, 0] > 0 and st[0, 1] >= st[0, 0] and st[0, 3] > 0
