@@ -228,7 +228,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     if ((rc = make_plan(h, w, r_last, mode, keep != nullptr, avoid != nullptr, fg, pl))) return rc;
     const int grid = (int)std::min<long long>(n, pl.per_wave);
     const size_t ws_words = (size_t)pl.stride * grid;
-    const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * 4 * sizeof(long long) : 0);
+    const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0);
     char *ctrl = nullptr;
     uint32_t *gws = nullptr;
     TS_CUDA(cudaMallocAsync((void **)&ctrl, ctrl_bytes, st));
@@ -270,7 +270,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     cudaError_t ce = cudaSuccess;
     if (le == cudaSuccess) ce = cudaMemcpyAsync(&herr, ctrl + 16, sizeof(int), cudaMemcpyDeviceToHost, st);
     if (le == cudaSuccess && ce == cudaSuccess && stats_host)
-        ce = cudaMemcpyAsync(stats_host, ctrl + 64, (size_t)n * 4 * sizeof(long long), cudaMemcpyDeviceToHost, st);
+        ce = cudaMemcpyAsync(stats_host, ctrl + 64, (size_t)n * kStatFields * sizeof(long long), cudaMemcpyDeviceToHost, st);
     if (gws) cudaFreeAsync(gws, st);
     cudaFreeAsync(ctrl, st);
     cudaError_t se = cudaStreamSynchronize(st);

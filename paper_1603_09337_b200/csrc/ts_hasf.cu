@@ -398,6 +398,8 @@ __device__ void rebuild(const Img &g, int t, int *counter) {
 
 struct Stats {
     long long sweeps, passes, calls;
+    long long cyc_prep, cyc_jacobi, cyc_update;   // thread-0 clock64 deltas (stats mode only)
+    bool timing;
 };
 
 // the priority-ordered flip engine (topo.py:211-258), see file header.
@@ -423,6 +425,7 @@ __device__ void engine(const Img &g, int t, long long max_sweeps, int *counters,
             break;
         }
         // chaotic fixpoint over this sweep's candidates
+        const long long tj0 = st.timing ? clock64() : 0;
         long long passes = 0;
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
         bool bad = false;
@@ -440,6 +443,7 @@ __device__ void engine(const Img &g, int t, long long max_sweeps, int *counters,
             if (threadIdx.x == 0) set_err(err, ERR_JACOBI_CAP);
             break;
         }
+        const long long tj1 = st.timing ? clock64() : 0;
         // apply the sweep's flips, mark the 3x3 word neighbourhoods dirty
         if (threadIdx.x == 0) counters[cur ^ 1] = 0;
         unsigned flips = 0;
@@ -471,6 +475,11 @@ __device__ void engine(const Img &g, int t, long long max_sweeps, int *counters,
         __syncthreads();
         ++sweeps;
         st.passes += passes;
+        if (st.timing) {
+            const long long tj2 = clock64();
+            st.cyc_jacobi += tj1 - tj0;
+            st.cyc_update += tj2 - tj1;
+        }
     }
     st.sweeps += sweeps;
     st.calls += 1;
@@ -480,10 +489,12 @@ template <int FG>
 __device__ void run_stage(const Img &g, int r, bool thin, int xmode, bool save_xs, int *counters, int &cur,
                           int *err, Stats &st, unsigned long long *s_flips) {
     if (threadIdx.x == 0) counters[cur] = 0;
+    const long long tp0 = st.timing ? clock64() : 0;
     const int S = prep_dispatch(r, g, thin, xmode, save_xs);
     __syncthreads();
     epass_ranks<FG>(g, S, thin ? 1 : 0, &counters[cur]);
     __syncthreads();
+    if (st.timing) st.cyc_prep += clock64() - tp0;
     engine<FG>(g, thin ? 1 : 0, -1, counters, cur, err, st, s_flips);
 }
 
@@ -560,7 +571,8 @@ __global__ void __launch_bounds__(kThreads, 1) hasf_kernel(const KParams p) {
         }
         __syncthreads();
 
-        Stats st{0, 0, 0};
+        Stats st{0, 0, 0, 0, 0, 0, p.stats != nullptr};
+        const long long t_img0 = st.timing ? clock64() : 0;
         int cur = 0;
         unsigned long long *fl = p.stats ? &s_flips : nullptr;
         if (p.mode == MODE_HASF) {
@@ -583,11 +595,15 @@ __global__ void __launch_bounds__(kThreads, 1) hasf_kernel(const KParams p) {
 
         unpack_plane(g.I, p.out + pix, g);
         if (threadIdx.x == 0 && p.stats) {
-            long long *sp = p.stats + (size_t)img * 4;
+            long long *sp = p.stats + (size_t)img * kStatFields;
             sp[0] = st.sweeps;
             sp[1] = st.passes;
             sp[2] = st.calls;
             sp[3] = (long long)s_flips;
+            sp[4] = st.cyc_prep;
+            sp[5] = st.cyc_jacobi;
+            sp[6] = st.cyc_update;
+            sp[7] = clock64() - t_img0;
         }
         __syncthreads();
     }

@@ -22,6 +22,11 @@ enum Buf : int {
     B_COUNT
 };
 
+// per-image stats: sweeps, fixpoint passes, engine calls, flips, and thread-0
+// clock64 cycles in prep (EDT/rank + E passes), fixpoint passes, apply+rebuild,
+// and the whole image (incl. pack/unpack)
+constexpr int kStatFields = 8;
+
 enum Mode : int { MODE_HASF = 0, MODE_THIN = 1, MODE_THICKEN = 2 };
 
 enum Err : int {
@@ -53,7 +58,7 @@ struct KParams {
     long long off[B_COUNT]; // word offset of each buffer (smem or CTA slice)
     int *counter;           // image queue head
     int *err;               // first error code (atomicCAS from 0)
-    long long *stats;       // [n][4]: sweeps, jacobi passes, engine calls, flips (or null)
+    long long *stats;       // [n][kStatFields] (or null), see kStatFields
 };
 
 }  // namespace ts

@@ -1,0 +1,58 @@
+"""Profiling driver: one fused-kernel launch over N images of a config, with
+per-image engine stats and thread-0 phase cycle counters.  Used under ncu
+(`-k regex:hasf_kernel -c 1`) and for quick phase breakdowns.
+
+    python tools/prof_hasf.py --config c1 --n 148 [--smem-budget B] [--repeat 3]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1603_09337_b200 import workloads as W  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--n", type=int, default=148)
+    ap.add_argument("--start", type=int, default=0)
+    ap.add_argument("--smem-budget", type=int, default=-1)
+    ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--stats", type=int, default=1)
+    args = ap.parse_args()
+    import torch
+    import paper_1603_09337_b200 as P
+    from paper_1603_09337_b200 import _lib
+    cfg = W.CONFIGS[args.config]
+    if args.smem_budget >= 0:
+        _lib.load().ts_set_smem_budget(args.smem_budget)
+    imgs = torch.from_numpy(W.config_batch(cfg, args.start, args.n)).cuda()
+    adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
+    plan = np.zeros(5, np.int64)
+    _lib.load().ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
+    res = {"config": cfg.name, "n": args.n, "plan": plan.tolist()}
+    for i in range(args.repeat):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if args.stats:
+            out, st = P.hasf_batch(imgs, cfg.r_max, adj, stats=True)
+        else:
+            out = P.hasf_batch(imgs, cfg.r_max, adj)
+        e1.record()
+        torch.cuda.synchronize()
+        res[f"ms_{i}"] = e0.elapsed_time(e1)
+    if args.stats:
+        m = st.mean(axis=0)
+        res.update({"sweeps": m[0], "passes": m[1], "calls": m[2], "flips": m[3],
+                    "cyc_prep": m[4], "cyc_jacobi": m[5], "cyc_update": m[6], "cyc_total": m[7],
+                    "cyc_total_max": int(st[:, 7].max()), "cyc_total_min": int(st[:, 7].min())})
+    print(json.dumps(res, default=float))
+
+
+if __name__ == "__main__":
+    main()
