@@ -50,9 +50,10 @@ int ts_max_radius(void);
 /* HASF: alternate homotopic cutting and filling at radii 1..r_max.
  * Replaces hasf(img, SmoothingConfig(r_max, adj, keep, avoid)) and smooth(img, r_max)
  * (smoothing.py:187-217).  keep_dev / avoid_dev: [n][h][w] constraint images or
- * NULL.  stats_host: NULL or int64[n*8] receiving per image: sweeps, fixpoint
+ * NULL.  stats_host: NULL or int64[n*16] receiving per image: sweeps, fixpoint
  * passes, engine calls, flips, then SM clock cycles spent in prep (clamped
- * EDT + precedence masks), fixpoint passes, apply+re-examination, and in total. */
+ * EDT + precedence masks), fixpoint passes, apply+re-examination, in total,
+ * and a breakdown by sweep size (fields 8-14; 15 reserved). */
 int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w,
                   int32_t r_max, int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev,
                   void *stream, int64_t *stats_host);

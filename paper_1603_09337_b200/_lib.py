@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtoposmooth_b200.so")
+LIB_PATH = os.environ.get("TS_LIB_PATH") or os.path.join(HERE, "libtoposmooth_b200.so")
 
 TS_OK, TS_ERR_VALUE, TS_ERR_CUDA, TS_ERR_INTERNAL, TS_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 
@@ -53,7 +53,7 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing:
+        if build_if_missing and not os.environ.get("TS_LIB_PATH"):
             from . import build as _build
             if _build.needs_build():
                 _build.build()

@@ -1,4 +1,5 @@
-"""Builds libtoposmooth_b200.so in-tree with nvcc for sm_100a.
+"""Builds libtoposmooth_b200.so in-tree with nvcc for sm_100a (translation
+units compiled in parallel, then linked).
 
     python -m paper_1603_09337_b200.build [--verbose]
 """
@@ -11,37 +12,70 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libtoposmooth_b200.so")
-SOURCES = ["ts_hasf.cu", "ts_edt.cu", "ts_api.cu"]
+SOURCES = ["ts_hasf_8h.cu", "ts_hasf_4h.cu", "ts_hasf_8g.cu", "ts_hasf_4g.cu", "ts_hasf.cu", "ts_edt.cu",
+           "ts_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+
+
+def _deps():
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(HERE, "..", "include", "toposmooth_b200.h"))
+    deps.append(os.path.abspath(__file__))
+    return [d for d in deps if os.path.exists(d)]
 
 
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(HERE, "..", "include", "toposmooth_b200.h"))
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile all translation units in parallel and link the shared library.
+    `defines` (e.g. ["TS_MIN_BLOCKS=1"]) and `out` build experiment variants."""
+    lib = out or LIB
+    if not force and not defines and out is None and not needs_build():
         return LIB
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "--expt-relaxed-constexpr", "-o", LIB]
-    if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    obj_dir = OBJ if not defines else OBJ + "_" + "_".join(d.replace("=", "") for d in defines)
+    os.makedirs(obj_dir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            cmd += ["-Xptxas", "-v"]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                                 text=True)))
+    objs, failed = [], []
+    for src, obj, p in procs:
+        out, _ = p.communicate()
+        if p.returncode != 0:
+            failed.append(src)
+            sys.stderr.write(out)
+        elif verbose:
+            sys.stderr.write(out)
+        objs.append(obj)
+    if failed:
+        raise RuntimeError(f"nvcc failed on {failed}")
+    tmp = lib + ".tmp"
+    res = subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libtoposmooth_b200.so")
-    if verbose:
-        sys.stderr.write(res.stdout + res.stderr)
-    return LIB
+        raise RuntimeError("nvcc link failed for libtoposmooth_b200.so")
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force=True))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--define", action="append", default=[])
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    print(build(verbose=a.verbose, force=True, defines=a.define, out=a.out))

@@ -20,7 +20,7 @@
 
 namespace ts {
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream);
-cudaError_t hasf_occupancy(int fg, size_t smem_bytes, int *blocks_per_sm);
+cudaError_t hasf_occupancy(int fg, bool hot, size_t smem_bytes, int *blocks_per_sm);
 int hasf_threads();
 cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
                               cudaStream_t st);
@@ -111,15 +111,17 @@ struct Plan {
     int per_sm = 0, per_wave = 0;
     size_t smem_bytes = 0;
     uint32_t mask = 0;
+    bool hot = false;
     long long off[B_COUNT] = {};
     long long stride = 0;   // global words per CTA
 };
 
-int device_props(int *sms, int *smem_optin) {
+int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
     int dev = 0;
     TS_CUDA(cudaGetDevice(&dev));
     TS_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
     TS_CUDA(cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    TS_CUDA(cudaDeviceGetAttribute(smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
     return TS_OK;
 }
 
@@ -134,8 +136,8 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     long long size[B_COUNT];
     size[B_I] = r4(nw);
     size[B_D] = r4(nw);
-    size[B_C] = r4(nw);
-    size[B_DIRTY] = r4(((nw + 15) / 16) * 4);
+    size[B_DIRTY] = r4((nw + 31) / 32);
+    size[B_MARK] = r4(((nw + 15) / 16) * 4);
     size[B_LIST] = r4(nw);
     size[B_E] = r4(8 * nw);
     size[B_B] = r4(nw);
@@ -144,12 +146,17 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     size[B_K] = (mode == MODE_HASF && has_k) ? r4(nw) : 0;
     size[B_A] = (mode == MODE_HASF && has_a) ? r4(nw) : 0;
 
-    int sms = 0, optin = 0;
-    int rc = device_props(&sms, &optin);
+    int sms = 0, optin = 0, per_sm = 0;
+    int rc = device_props(&sms, &optin, &per_sm);
     if (rc) return rc;
-    long long budget = optin - 256;   // static shared scalars of the kernel
+    // default: two resident images per SM when the hot planes fit in half an
+    // SM's shared memory (1 KB per-CTA reservation + static scalars), else one
+    long long budget = optin - 256;
+    const long long hot_bytes = 4 * (size[B_I] + size[B_D] + size[B_B] + size[B_DIRTY] + size[B_MARK]);
+    const long long half = per_sm / 2 - 1024 - 256;
+    if (hot_bytes <= half) budget = half;
     const long long knob = g_smem_budget.load();
-    if (knob > 0 && knob < budget) budget = knob;
+    if (knob > 0 && knob < optin - 256) budget = knob;
     long long used = 0, gused = 0;
     pl.mask = 0;
     for (int b = 0; b < B_COUNT; ++b) {
@@ -167,12 +174,14 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         }
     }
     pl.smem_bytes = (size_t)(used * 4);
+    const uint32_t hot_mask = (1u << B_I) | (1u << B_D) | (1u << B_B) | (1u << B_DIRTY) | (1u << B_MARK);
+    pl.hot = (pl.mask & hot_mask) == hot_mask;
     pl.stride = gused;
-    int per_sm = 0;
-    TS_CUDA(hasf_occupancy(fg, pl.smem_bytes, &per_sm));
-    if (per_sm < 1) return fail(TS_ERR_CUDA, "fused kernel does not fit on an SM");
-    pl.per_sm = per_sm;
-    pl.per_wave = per_sm * sms;
+    int blocks = 0;
+    TS_CUDA(hasf_occupancy(fg, pl.hot, pl.smem_bytes, &blocks));
+    if (blocks < 1) return fail(TS_ERR_CUDA, "fused kernel does not fit on an SM");
+    pl.per_sm = blocks;
+    pl.per_wave = blocks * sms;
     return TS_OK;
 }
 
@@ -261,6 +270,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     p.gws = gws;
     p.gws_stride = pl.stride;
     p.smem_mask = pl.mask;
+    p.hot = pl.hot ? 1 : 0;
     for (int b = 0; b < B_COUNT; ++b) p.off[b] = pl.off[b];
     p.counter = reinterpret_cast<int *>(ctrl);
     p.err = reinterpret_cast<int *>(ctrl + 16);

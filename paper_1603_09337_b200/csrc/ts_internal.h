@@ -9,12 +9,12 @@ namespace ts {
 // (L2-resident); the host places them greedily in this priority order.
 enum Buf : int {
     B_I = 0,     // current image, bit-packed                          nwords
-    B_D,         // Jacobi decisions of the current sweep              nwords
-    B_C,         // candidates of the current sweep                    nwords
-    B_DIRTY,     // per-word "re-examine" flags (bytes)                ceil16(nwords)/4
+    B_D,         // fixpoint decisions of the current sweep            nwords
+    B_B,         // blocked (floor) plane                              nwords
+    B_DIRTY,     // "re-examine" bitmap, 1 bit per word                ceil(nwords/32)
+    B_MARK,      // per-word pass stamps of the fixpoint worklist      nwords bytes
     B_LIST,      // active-word list, (y << 16) | x                    nwords
     B_E,         // 8 "earlier neighbour" masks per word, interleaved  8 * nwords
-    B_B,         // blocked (floor) plane                              nwords
     B_XS,        // saved image (cutting input X / filling input X')   nwords
     B_R,         // rank bit-slices of the clamped distance map        S * nwords
     B_K,         // keep constraint plane (optional)                   nwords
@@ -22,10 +22,12 @@ enum Buf : int {
     B_COUNT
 };
 
-// per-image stats: sweeps, fixpoint passes, engine calls, flips, and thread-0
-// clock64 cycles in prep (EDT/rank + E passes), fixpoint passes, apply+rebuild,
-// and the whole image (incl. pack/unpack)
-constexpr int kStatFields = 8;
+// per-image stats: 0 sweeps, 1 fixpoint passes, 2 engine calls, 3 flips, then
+// thread-0 clock64 cycles: 4 prep (EDT/rank + E passes), 5 fixpoint passes,
+// 6 apply+rebuild, 7 whole image (incl. pack/unpack); 8-10 cycles / sweeps /
+// passes of tiny sweeps (<= 32 words), 11-13 the same for dense sweeps
+// (> one word per thread), 14 cycles of the clamped-EDT part of prep
+constexpr int kStatFields = 16;
 
 enum Mode : int { MODE_HASF = 0, MODE_THIN = 1, MODE_THICKEN = 2 };
 
@@ -55,6 +57,7 @@ struct KParams {
     uint32_t *gws;          // global workspace, gws_stride words per CTA
     long long gws_stride;
     uint32_t smem_mask;     // bit b set: buffer b lives in shared memory
+    int hot;                // I, D, B, DIRTY, MARK all in shared memory (fast variant)
     long long off[B_COUNT]; // word offset of each buffer (smem or CTA slice)
     int *counter;           // image queue head
     int *err;               // first error code (atomicCAS from 0)

@@ -114,8 +114,9 @@ def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=Non
     torch CUDA tensors stay on the device (returns a CUDA uint8 tensor); numpy
     input returns numpy.  Input/constraint validation happens on the device
     and raises ValueError with the reference's messages.  With stats=True also
-    returns an int64 [n, 8] array: sweeps, fixpoint passes, engine calls, flips,
-    cycles in prep / fixpoint passes / apply+re-examination / total.
+    returns an int64 [n, 16] array: sweeps, fixpoint passes, engine calls, flips,
+    cycles in prep / fixpoint passes / apply+re-examination / total, then
+    tiny-sweep and dense-sweep breakdowns (see csrc/ts_internal.h kStatFields).
     """
     import torch
     r_max = _check_radius(r_max)
@@ -130,7 +131,7 @@ def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=Non
         if t is not None and tuple(t.shape) != (n, h, w):
             raise ValueError(f"{name} constraint shape {tuple(t.shape)} != batch shape {(n, h, w)}")
     out = torch.empty_like(x)
-    st = np.zeros((n, 8), np.int64) if stats else None
+    st = np.zeros((n, 16), np.int64) if stats else None
     check(load().ts_hasf_batch(x.data_ptr(), out.data_ptr(), n, h, w, r_max, adj.fg, D.ptr(k), D.ptr(a),
                                D.stream_ptr(), None if st is None else st.ctypes.data))
     res = out.cpu().numpy() if is_numpy else out

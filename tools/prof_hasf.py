@@ -50,7 +50,9 @@ def main():
         m = st.mean(axis=0)
         res.update({"sweeps": m[0], "passes": m[1], "calls": m[2], "flips": m[3],
                     "cyc_prep": m[4], "cyc_jacobi": m[5], "cyc_update": m[6], "cyc_total": m[7],
-                    "cyc_total_max": int(st[:, 7].max()), "cyc_total_min": int(st[:, 7].min())})
+                    "cyc_total_max": int(st[:, 7].max()), "cyc_total_min": int(st[:, 7].min()),
+                    "cyc_tiny": m[8], "n_tiny": m[9], "pass_tiny": m[10], "cyc_dense": m[11], "n_dense": m[12],
+                    "pass_dense": m[13], "cyc_rank": m[14], "evals": m[15]})
     print(json.dumps(res, default=float))
 
 
