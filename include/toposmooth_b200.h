@@ -124,6 +124,10 @@ int ts_selftest_circuit(uint8_t *s84_256_host, uint8_t *s48_256_host);
  * buffers; 0 = device maximum.  Returns the previous value. */
 int64_t ts_set_smem_budget(int64_t bytes);
 
+/* Tuning: a sweep runs in dense (strip-walk) mode when more than
+ * (words / div) words hold candidates (default div = 8).  Returns the previous value. */
+int32_t ts_set_dense_divisor(int32_t div);
+
 /* Placement/occupancy the fused kernel would use for an image shape:
  * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
  * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA. */

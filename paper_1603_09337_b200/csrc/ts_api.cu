@@ -7,6 +7,7 @@
 // (nothing is ever returned silently wrong).  No global mutable state besides
 // the thread-local error string and the shared-memory budget knob.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <atomic>
 #include <climits>
 #include <cstdint>
@@ -108,13 +109,52 @@ const Tables &tables() {
 // ---- fused-kernel planning ------------------------------------------------
 struct Plan {
     int WW = 0, nwords = 0, slices = 0;
+    int stride = 0, plen = 0, nblk = 1, hb = 1, dense_min = 0;
     int per_sm = 0, per_wave = 0;
     size_t smem_bytes = 0;
     uint32_t mask = 0;
     bool hot = false;
     long long off[B_COUNT] = {};
-    long long stride = 0;   // global words per CTA
+    long long stride_ws = 0;   // global workspace words per CTA
 };
+
+std::atomic<int> g_dense_div{8};
+
+// strip mapping (thread t -> word column t % WW, row block t / WW) and the
+// padded row stride that puts the 32 lanes of every warp on distinct banks
+void plan_strips(int H, int WW, int threads, Plan &pl) {
+    if (WW > threads) {
+        pl.nblk = 1;
+        pl.hb = H;
+        pl.stride = WW + 1;
+        return;
+    }
+    int nblk = std::min(threads / WW, H);
+    const int hb = (H + nblk - 1) / nblk;
+    nblk = (H + hb - 1) / hb;
+    pl.nblk = nblk;
+    pl.hb = hb;
+    const int active = nblk * WW;
+    int best_s = WW + 1, best_cost = 1 << 30;
+    for (int S = WW + 1; S <= WW + 64; ++S) {
+        int cost = 0;
+        for (int w0 = 0; w0 < active; w0 += 32) {
+            int cnt[32] = {0};
+            int worst = 0;
+            for (int t = w0; t < std::min(active, w0 + 32); ++t) {
+                const long long a = (long long)(t / WW) * hb * S + (t % WW);
+                worst = std::max(worst, ++cnt[a & 31]);
+            }
+            cost = std::max(cost, worst);
+        }
+        if (cost < best_cost) {
+            best_cost = cost;
+            best_s = S;
+        }
+        if (best_cost == 1) break;
+    }
+    pl.stride = best_s;
+}
 
 int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
     int dev = 0;
@@ -127,36 +167,37 @@ int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
 
 int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl) {
     pl.WW = (W + 31) / 32;
-    const long long nw = (long long)H * pl.WW;
-    if (H >= 65536 || pl.WW >= 65536 || nw * 8 >= (long long)INT_MAX)
-        return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel (h < 65536, w < 2^21, h*w/32*8 < 2^31)");
-    pl.nwords = (int)nw;
+    if (H >= (1 << 20) || pl.WW >= (1 << 16))
+        return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");
+    plan_strips(H, pl.WW, hasf_threads(), pl);
+    const long long plen = (((long long)H + 2 * kPadRows) * pl.stride + 4 + 3) & ~3LL;
+    if (plen * 8 >= (long long)INT_MAX)
+        return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel (padded plane * 8 >= 2^31 words)");
+    pl.plen = (int)plen;
+    pl.nwords = H * pl.WW;
+    pl.dense_min = pl.nwords / std::max(1, g_dense_div.load());
     pl.slices = (mode == MODE_HASF && r_last >= 1) ? rank_slices(r_last) : 0;
     auto r4 = [](long long x) { return (x + 3) & ~3LL; };
     long long size[B_COUNT];
-    size[B_I] = r4(nw);
-    size[B_D] = r4(nw);
-    size[B_DIRTY] = r4((nw + 31) / 32);
-    size[B_MARK] = r4(((nw + 15) / 16) * 4);
-    size[B_LIST] = r4(nw);
-    size[B_E] = r4(8 * nw);
-    size[B_B] = r4(nw);
-    size[B_XS] = mode == MODE_HASF ? r4(nw) : 0;
-    size[B_R] = r4((long long)pl.slices * nw);
-    size[B_K] = (mode == MODE_HASF && has_k) ? r4(nw) : 0;
-    size[B_A] = (mode == MODE_HASF && has_a) ? r4(nw) : 0;
+    size[B_I] = plen;
+    size[B_D] = plen;
+    size[B_C] = plen;
+    size[B_B] = plen;
+    size[B_DIRTY] = r4((plen + 31) / 32);
+    size[B_MARK] = r4(((plen + 15) / 16) * 4);
+    size[B_LIST] = plen;
+    size[B_E] = 8 * plen;
+    size[B_XS] = mode == MODE_HASF ? plen : 0;
+    size[B_R] = (long long)pl.slices * plen;
+    size[B_K] = (mode == MODE_HASF && has_k) ? plen : 0;
+    size[B_A] = (mode == MODE_HASF && has_a) ? plen : 0;
 
     int sms = 0, optin = 0, per_sm = 0;
     int rc = device_props(&sms, &optin, &per_sm);
     if (rc) return rc;
-    // default: two resident images per SM when the hot planes fit in half an
-    // SM's shared memory (1 KB per-CTA reservation + static scalars), else one
-    long long budget = optin - 256;
-    const long long hot_bytes = 4 * (size[B_I] + size[B_D] + size[B_B] + size[B_DIRTY] + size[B_MARK]);
-    const long long half = per_sm / 2 - 1024 - 256;
-    if (hot_bytes <= half) budget = half;
+    long long budget = optin - 512;   // static shared scalars of the kernel
     const long long knob = g_smem_budget.load();
-    if (knob > 0 && knob < optin - 256) budget = knob;
+    if (knob > 0 && knob < budget) budget = knob;
     long long used = 0, gused = 0;
     pl.mask = 0;
     for (int b = 0; b < B_COUNT; ++b) {
@@ -174,9 +215,10 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         }
     }
     pl.smem_bytes = (size_t)(used * 4);
-    const uint32_t hot_mask = (1u << B_I) | (1u << B_D) | (1u << B_B) | (1u << B_DIRTY) | (1u << B_MARK);
+    pl.stride_ws = gused;
+    const uint32_t hot_mask =
+        (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_B) | (1u << B_DIRTY) | (1u << B_MARK);
     pl.hot = (pl.mask & hot_mask) == hot_mask;
-    pl.stride = gused;
     int blocks = 0;
     TS_CUDA(hasf_occupancy(fg, pl.hot, pl.smem_bytes, &blocks));
     if (blocks < 1) return fail(TS_ERR_CUDA, "fused kernel does not fit on an SM");
@@ -236,7 +278,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     Plan pl;
     if ((rc = make_plan(h, w, r_last, mode, keep != nullptr, avoid != nullptr, fg, pl))) return rc;
     const int grid = (int)std::min<long long>(n, pl.per_wave);
-    const size_t ws_words = (size_t)pl.stride * grid;
+    const size_t ws_words = (size_t)pl.stride_ws * grid;
     const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0);
     char *ctrl = nullptr;
     uint32_t *gws = nullptr;
@@ -268,7 +310,12 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     p.max_sweeps = max_sweeps;
     p.slices = pl.slices;
     p.gws = gws;
-    p.gws_stride = pl.stride;
+    p.gws_stride = pl.stride_ws;
+    p.stride = pl.stride;
+    p.plen = pl.plen;
+    p.nblk = pl.nblk;
+    p.hb = pl.hb;
+    p.dense_min = pl.dense_min;
     p.smem_mask = pl.mask;
     p.hot = pl.hot ? 1 : 0;
     for (int b = 0; b < B_COUNT; ++b) p.off[b] = pl.off[b];
@@ -306,6 +353,8 @@ int ts_max_radius(void) { return kMaxR; }
 
 int64_t ts_set_smem_budget(int64_t bytes) { return g_smem_budget.exchange(bytes < 0 ? 0 : bytes); }
 
+int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 1 ? 1 : div); }
+
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {
     int rc;
     if ((rc = check_shape(1, h, w))) return rc;
@@ -315,7 +364,7 @@ int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t 
     info5[1] = pl.per_sm;
     info5[2] = (int64_t)pl.smem_bytes;
     info5[3] = pl.mask;
-    info5[4] = pl.stride * 4;
+    info5[4] = pl.stride_ws * 4;
     return ok();
 }
 

@@ -1,4 +1,5 @@
-// Fused per-image HASF kernel for sm_100a.
+// Fused per-image HASF kernel for sm_100a (body; instantiated per variant in
+// ts_hasf_<fg><h|g>.cu).
 //
 // One persistent CTA owns one image at a time (images are pulled from an
 // atomic queue, so uneven per-image work balances across SMs) and runs the
@@ -24,17 +25,27 @@
 // by a chaotic fixpoint over the sweep's candidates: pixel p
 // flips iff SIMPLE(code of p with every candidate neighbour q that precedes p
 // in key order toggled iff q flips).  The precedence masks ("E" planes) are
-// computed once per engine call from the rank slices; a pass with no change
-// certifies the unique solution.  Later sweeps only re-examine the 3x3 word
-// neighbourhood of the previous sweep's flips (the reference's re-queue,
-// topo.py:245-257), found through a 1-bit-per-word dirty bitmap.
+// computed once per engine call from the rank slices.  Any evaluation order
+// reaches the unique solution; a pass in which no decision changes certifies
+// it.  Two sweep modes:
+//   dense  (many candidates): every thread walks its vertical strip of words
+//          with a sliding 3-row register window (updates propagate down the
+//          strip within a pass), candidates kept in the C plane;
+//   sparse (few candidates): an active-word list, the thread's first word's
+//          sweep-constant data cached in registers, one warp only when <= 32
+//          words; the next sweep re-examines only the 3x3 word neighbourhoods
+//          of the flips (the reference's re-queue, topo.py:245-257) found
+//          through a 1-bit-per-word dirty bitmap.
+// After the first pass of a sweep only words stamped by a changed neighbour
+// decision are re-evaluated (a worklist of per-word pass stamps).
 //
-// Memory: the hot planes (image I, decisions D, candidates C, blocked B, the
-// dirty bitmap and the active-word list) live in shared memory whenever they
-// fit (the HOT variant; accessed as true LDS/STS); the E planes, rank slices
-// and saved image go to shared memory if space remains, else to the CTA's
-// slice of an L2-resident global workspace.  Thread <-> word mappings are
-// always lane-consecutive, so neighbour-word loads are bank-conflict free.
+// Layout: every plane is padded with kPadRows zero rows above and below and
+// one zero word between rows (row stride S >= WW + 1, chosen on the host so
+// the 32 lanes of a warp touch 32 distinct banks), so neighbour and disc
+// accesses need no bounds checks.  The hot planes (I, D, C, B, the dirty
+// bitmap and the stamps) live in shared memory when they fit (HOT variant,
+// accessed as LDS/STS); E, rank slices, saved image, list spill to the CTA's
+// slice of an L2-resident global workspace when shared memory runs out.
 #pragma once
 #include <cuda_runtime.h>
 #include "ts_common.cuh"
@@ -50,61 +61,56 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMinBlocks = TS_MIN_BLOCKS;   // resident images per SM the register budget targets
 
 struct Img {
-    uint32_t *I, *D, *B, *dirty;              // hot planes
-    uint8_t *mark;                            // hot: fixpoint worklist stamps
-    uint32_t *list, *E, *XS, *R, *K, *A;      // smem or global
-    int H, W, WW, nwords;
+    uint32_t *I, *D, *C, *B, *dirty;      // hot planes
+    uint8_t *mark;                        // hot: worklist pass stamps
+    uint32_t *list, *E, *XS, *R, *K, *A;  // smem or global
+    int H, W, WW;
+    int S;          // padded row stride (words)
+    int plen;       // padded plane length (words)
+    int org;        // index of word (0, 0)
     uint32_t lastmask;   // valid bits of the last word of a row
-    int ww_shift;        // log2(WW) if WW is a power of two, else -1
+    int nblk, hb;        // strip mapping: row blocks per column, rows per block
+    int dense_min;       // sweeps with more listed words run in dense mode
 };
 
+__device__ __forceinline__ int pidx(const Img &g, int y, int x) { return g.org + y * g.S + x; }
+
 __device__ __forceinline__ void set_err(int *err, int code) { atomicCAS(err, 0, code); }
-
-__device__ __forceinline__ uint32_t valid_bits(const Img &g, int x) { return x == g.WW - 1 ? g.lastmask : ~0u; }
-
-__device__ __forceinline__ void word_yx(const Img &g, int w, int &y, int &x) {
-    if (g.ww_shift >= 0) {
-        y = w >> g.ww_shift;
-        x = w & (g.WW - 1);
-    } else {
-        y = w / g.WW;
-        x = w - y * g.WW;
-    }
-}
-
-__device__ __forceinline__ uint32_t ldw(const uint32_t *P, const Img &g, int y, int x) {
-    return (y < 0 || y >= g.H || x < 0 || x >= g.WW) ? 0u : P[y * g.WW + x];
-}
 
 struct Nb {
     uint32_t nw, n, ne, w, e, sw, s, se;
     uint32_t m;   // the centre word itself
 };
 
-__device__ __forceinline__ Nb shifts(uint32_t u0, uint32_t u1, uint32_t u2, uint32_t m0, uint32_t m1, uint32_t m2,
-                                     uint32_t d0, uint32_t d1, uint32_t d2) {
+// neighbour bit-words of the 32 pixels of padded word p (pads read as 0)
+__device__ __forceinline__ Nb nbrs(const uint32_t *P, const Img &g, int p) {
+    const uint32_t *u = P + p - g.S, *m = P + p, *d = P + p + g.S;
     Nb r;
-    r.nw = from_west(u0, u1);
-    r.n = u1;
-    r.ne = from_east(u1, u2);
-    r.w = from_west(m0, m1);
-    r.e = from_east(m1, m2);
-    r.sw = from_west(d0, d1);
-    r.s = d1;
-    r.se = from_east(d1, d2);
-    r.m = m1;
+    r.nw = from_west(u[-1], u[0]);
+    r.n = u[0];
+    r.ne = from_east(u[0], u[1]);
+    r.w = from_west(m[-1], m[0]);
+    r.e = from_east(m[0], m[1]);
+    r.sw = from_west(d[-1], d[0]);
+    r.s = d[0];
+    r.se = from_east(d[0], d[1]);
+    r.m = m[0];
     return r;
 }
 
-// neighbour bit-words of the 32 pixels of word (y, x); outside the window = 0
-__device__ __forceinline__ Nb nbrs(const uint32_t *P, const Img &g, int y, int x) {
-    const bool up = y > 0, dn = y + 1 < g.H, lf = x > 0, rt = x + 1 < g.WW;
-    const uint32_t *row = P + y * g.WW + x;
-    const uint32_t u1 = up ? row[-g.WW] : 0u, d1 = dn ? row[g.WW] : 0u, m1 = row[0];
-    const uint32_t u0 = (up && lf) ? row[-g.WW - 1] : 0u, u2 = (up && rt) ? row[-g.WW + 1] : 0u;
-    const uint32_t m0 = lf ? row[-1] : 0u, m2 = rt ? row[1] : 0u;
-    const uint32_t d0 = (dn && lf) ? row[g.WW - 1] : 0u, d2 = (dn && rt) ? row[g.WW + 1] : 0u;
-    return shifts(u0, u1, u2, m0, m1, m2, d0, d1, d2);
+// calls f(y, x, p) for the words of this thread's vertical strip, top to bottom
+template <class F>
+__device__ __forceinline__ void for_strip(const Img &g, F &&f) {
+    const int t = threadIdx.x;
+    if (g.WW <= kThreads) {
+        const int x = t % g.WW, blk = t / g.WW;
+        if (blk >= g.nblk) return;
+        const int y0 = blk * g.hb, y1 = min(g.H, y0 + g.hb);
+        for (int y = y0; y < y1; ++y) f(y, x, pidx(g, y, x));
+    } else {
+        for (int x = t; x < g.WW; x += kThreads)
+            for (int y = 0; y < g.H; ++y) f(y, x, pidx(g, y, x));
+    }
 }
 
 // ---- bit packing of uint8 {0,1} images ---------------------------------
@@ -123,39 +129,35 @@ __device__ __forceinline__ uint32_t spread4(uint32_t nib) {
 
 // pack one [H,W] uint8 image into a bit-plane; flags bytes > 1
 __device__ __forceinline__ void pack_plane(const uint8_t *src, uint32_t *dst, const Img &g, int *err, int code) {
-    for (int w = threadIdx.x; w < g.nwords; w += kThreads) {
-        int y, x;
-        word_yx(g, w, y, x);
+    for_strip(g, [&](int y, int x, int p) {
         const int c0 = x * 32;
         const int cnt = min(32, g.W - c0);
-        const uint8_t *p = src + (size_t)y * g.W + c0;
+        const uint8_t *s = src + (size_t)y * g.W + c0;
         uint32_t bits = 0, bad = 0;
-        if (cnt == 32 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p));
-            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(p + 16));
+        if (cnt == 32 && ((reinterpret_cast<uintptr_t>(s) & 15) == 0)) {
+            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(s));
+            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(s + 16));
             bits = pack16(a) | (pack16(b) << 16);
             bad = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0xFEFEFEFEu;
         } else {
             for (int i = 0; i < cnt; ++i) {
-                const uint32_t v = p[i];
+                const uint32_t v = s[i];
                 bits |= (v & 1u) << i;
                 bad |= v & ~1u;
             }
         }
         if (bad) set_err(err, code);
-        dst[w] = bits;
-    }
+        dst[p] = bits;
+    });
 }
 
 __device__ __forceinline__ void unpack_plane(const uint32_t *src, uint8_t *dst, const Img &g) {
-    for (int w = threadIdx.x; w < g.nwords; w += kThreads) {
-        int y, x;
-        word_yx(g, w, y, x);
+    for_strip(g, [&](int y, int x, int p) {
         const int c0 = x * 32;
         const int cnt = min(32, g.W - c0);
-        uint8_t *p = dst + (size_t)y * g.W + c0;
-        const uint32_t bits = src[w];
-        if (cnt == 32 && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+        uint8_t *d = dst + (size_t)y * g.W + c0;
+        const uint32_t bits = src[p];
+        if (cnt == 32 && ((reinterpret_cast<uintptr_t>(d) & 15) == 0)) {
             uint4 a, b;
             a.x = spread4(bits);
             a.y = spread4(bits >> 4);
@@ -165,36 +167,37 @@ __device__ __forceinline__ void unpack_plane(const uint32_t *src, uint8_t *dst, 
             b.y = spread4(bits >> 20);
             b.z = spread4(bits >> 24);
             b.w = spread4(bits >> 28);
-            reinterpret_cast<uint4 *>(p)[0] = a;
-            reinterpret_cast<uint4 *>(p)[1] = b;
+            reinterpret_cast<uint4 *>(d)[0] = a;
+            reinterpret_cast<uint4 *>(d)[1] = b;
         } else {
-            for (int i = 0; i < cnt; ++i) p[i] = (bits >> i) & 1u;
+            for (int i = 0; i < cnt; ++i) d[i] = (bits >> i) & 1u;
         }
-    }
+    });
 }
 
-// warp-aggregated append to the active-word list (all 32 lanes must call);
-// entries keep lane order, so a warp's entries are consecutive words
+// warp-aggregated append to the active-word list among the currently active
+// lanes (entries of one aggregate are consecutive in the list)
 __device__ __forceinline__ void append(bool has, uint32_t entry, uint32_t *list, int *counter) {
-    const unsigned m = __ballot_sync(0xffffffffu, has);
+    const unsigned act = __activemask();
+    const unsigned m = __ballot_sync(act, has);
     if (m == 0) return;
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(m) - 1;
     int base = 0;
     if (lane == leader) base = atomicAdd(counter, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
+    base = __shfl_sync(act, base, leader);
     if (has) list[base + __popc(m & ((1u << lane) - 1u))] = entry;
 }
 
-// candidates of word (y,x): target-valued, unblocked, simple (topo.py:186-208,
-// smoothing.py:83-86); t = 1 thins, t = 0 thickens
+// candidates of padded word p: target-valued, unblocked, simple
+// (topo.py:186-208, smoothing.py:83-86); t = 1 thins, t = 0 thickens (SURVEY
+// A.2.2).  Padding bits and pad words are blocked in B.
 template <int FG>
-__device__ __forceinline__ uint32_t cand_word(const Img &g, int y, int x, int t) {
-    const int w = y * g.WW + x;
-    const uint32_t me = g.I[w];
-    const uint32_t pre = valid_bits(g, x) & (t ? me : ~me) & ~g.B[w];
+__device__ __forceinline__ uint32_t cand_word(const Img &g, int p, int t) {
+    const uint32_t me = g.I[p];
+    const uint32_t pre = (t ? me : ~me) & ~g.B[p];
     if (!pre) return 0;
-    const Nb i = nbrs(g.I, g, y, x);
+    const Nb i = nbrs(g.I, g, p);
     return pre & simple_bits<FG>(i.nw, i.n, i.ne, i.w, i.e, i.sw, i.s, i.se);
 }
 
@@ -221,6 +224,7 @@ struct Lev {
 
 // thin = true : seeds = background + window exterior  (P for thinning, S1/S7)
 // thin = false: seeds = object pixels                  (D for thickening, S3/S5)
+// (the zero pads and padding bits make ~I the exterior seed automatically)
 // xmode (thin) : 0 -> F = P > r^2 ; 1 -> | keep ; 2 -> | XS
 // xmode (thick): 0 -> V = D <= r^2 ; 1 -> & ~avoid ; 2 -> & XS
 template <int R>
@@ -228,33 +232,21 @@ __device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, boo
     using LV = Lev<R>;
     constexpr int L = LV::L;
     constexpr int S = LV::S;
+    static_assert(R <= kPadRows, "disc rows must stay inside the padded frame");
     const uint32_t inv = thin ? ~0u : 0u;
-    for (int w = threadIdx.x; w < g.nwords; w += kThreads) {
-        int y, x;
-        word_yx(g, w, y, x);
-        const bool lf = x > 0, rt = x + 1 < g.WW;
-        const uint32_t padl = inv, padr = (thin && x + 2 == g.WW) ? ~g.lastmask : 0u;
-        const uint32_t padc = (thin && x + 1 == g.WW) ? ~g.lastmask : 0u;
-        auto seed3 = [&](int yy, uint32_t &a, uint32_t &b, uint32_t &c) {
-            if (yy < 0 || yy >= g.H) {
-                a = b = c = inv;
-                return;
-            }
-            const uint32_t *row = g.I + yy * g.WW + x;
-            a = lf ? (row[-1] ^ inv) : padl;
-            b = (row[0] ^ inv) | padc;
-            c = rt ? ((row[1] ^ inv) | padr) : inv;
-        };
+    const int SS = g.S;
+    for_strip(g, [&](int y, int x, int p) {
+        const uint32_t *c = g.I + p;
         uint32_t V[R + 1][3];
-        seed3(y, V[0][0], V[0][1], V[0][2]);
+        V[0][0] = c[-1] ^ inv;
+        V[0][1] = c[0] ^ inv;
+        V[0][2] = c[1] ^ inv;
 #pragma unroll
         for (int k = 1; k <= R; ++k) {
-            uint32_t a0, a1, a2, b0, b1, b2;
-            seed3(y - k, a0, a1, a2);
-            seed3(y + k, b0, b1, b2);
-            V[k][0] = V[k - 1][0] | a0 | b0;
-            V[k][1] = V[k - 1][1] | a1 | b1;
-            V[k][2] = V[k - 1][2] | a2 | b2;
+            const uint32_t *a = c - k * SS, *b = c + k * SS;
+            V[k][0] = V[k - 1][0] | (a[-1] ^ inv) | (b[-1] ^ inv);
+            V[k][1] = V[k - 1][1] | (a[0] ^ inv) | (b[0] ^ inv);
+            V[k][2] = V[k - 1][2] | (a[1] ^ inv) | (b[1] ^ inv);
         }
         uint32_t dil = 0, prev = 0;
         uint32_t rs[S];
@@ -285,25 +277,390 @@ __device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, boo
         // dil = pixels whose clamped distance is <= r^2
         uint32_t blocked;
         if (thin) {
-            const uint32_t extra = xmode == 1 ? g.K[w] : (xmode == 2 ? g.XS[w] : 0u);
+            const uint32_t extra = xmode == 1 ? g.K[p] : (xmode == 2 ? g.XS[p] : 0u);
             blocked = ~dil | extra;
         } else {
-            const uint32_t m = xmode == 1 ? ~g.A[w] : (xmode == 2 ? g.XS[w] : ~0u);
+            const uint32_t m = xmode == 1 ? ~g.A[p] : (xmode == 2 ? g.XS[p] : ~0u);
             blocked = ~(dil & m);
         }
-        g.B[w] = blocked | ~valid_bits(g, x);
+        g.B[p] = blocked | (x == g.WW - 1 ? ~g.lastmask : 0u);
 #pragma unroll
-        for (int s = 0; s < S; ++s) g.R[(size_t)s * g.nwords + w] = rs[s];
-        if (save_xs) g.XS[w] = g.I[w];
-    }
+        for (int s = 0; s < S; ++s) g.R[(size_t)s * g.plen + p] = rs[s];
+        if (save_xs) g.XS[p] = c[0];
+    });
     return S;
 }
 
-__device__ __forceinline__ int prep_dispatch(int r, const Img &g, bool thin, int xmode, bool save_xs) {
+static_assert(kMaxR == 16, "prep_dispatch covers radii 1..16");
+
+__device__ __forceinline__ void cmp_step(uint32_t &lt, uint32_t &eq, uint32_t nb, uint32_t own) {
+    lt |= eq & ~nb & own;   // neighbour < own at the first differing slice
+    eq &= ~(nb ^ own);
+}
+
+// E planes from rank slices + the sweep-1 candidates (C, D = C, list).
+// E_k(p) = key(q) < key(p) for q = neighbour k, key = (rank, raster index)
+// (topo.py:225,256): ties go to the raster-earlier neighbours NW,N,NE,W.
+template <int FG, int S>
+__device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
+    for_strip(g, [&](int y, int x, int p) {
+        uint32_t c = 0;
+        if (~g.B[p]) {
+            c = cand_word<FG>(g, p, t);
+            uint32_t lt[8], eq[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                lt[k] = 0;
+                eq[k] = ~0u;
+            }
+            Nb nbs[S];   // all slices' loads issued together (one L2 round trip)
+#pragma unroll
+            for (int s = 0; s < S; ++s) nbs[s] = nbrs(g.R + (size_t)s * g.plen, g, p);
+#pragma unroll
+            for (int s = S - 1; s >= 0; --s) {
+                const Nb &nb = nbs[s];
+                const uint32_t own = nb.m;
+                cmp_step(lt[0], eq[0], nb.nw, own);
+                cmp_step(lt[1], eq[1], nb.n, own);
+                cmp_step(lt[2], eq[2], nb.ne, own);
+                cmp_step(lt[3], eq[3], nb.w, own);
+                cmp_step(lt[4], eq[4], nb.e, own);
+                cmp_step(lt[5], eq[5], nb.sw, own);
+                cmp_step(lt[6], eq[6], nb.s, own);
+                cmp_step(lt[7], eq[7], nb.se, own);
+            }
+            uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
+            ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
+            ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
+        }
+        g.C[p] = c;
+        g.D[p] = c;
+        append(c != 0, (uint32_t)p, g.list, counter);
+    });
+}
+
+// E planes straight from an int64 priority map (public homotopic_thin /
+// homotopic_thicken: arbitrary priorities, topo.py:303-342)
+template <int FG>
+__device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, int t, int *counter) {
+    const int dy[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+    const int dx[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+    for_strip(g, [&](int y, int x, int p) {
+        uint32_t c = 0;
+        if (~g.B[p]) {
+            uint32_t e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const int cnt = min(32, g.W - x * 32);
+            for (int i = 0; i < cnt; ++i) {
+                const int col = x * 32 + i;
+                const int64_t pv = prio[(size_t)y * g.W + col];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int ny = y + dy[k], nc = col + dx[k];
+                    if (ny < 0 || ny >= g.H || nc < 0 || nc >= g.W) continue;
+                    const int64_t q = prio[(size_t)ny * g.W + nc];
+                    if (q < pv || (q == pv && k < 4)) e[k] |= 1u << i;
+                }
+            }
+            uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
+            ep[0] = make_uint4(e[0], e[1], e[2], e[3]);
+            ep[1] = make_uint4(e[4], e[5], e[6], e[7]);
+            c = cand_word<FG>(g, p, t);
+        }
+        g.C[p] = c;
+        g.D[p] = c;
+        append(c != 0, (uint32_t)p, g.list, counter);
+    });
+}
+
+__device__ __forceinline__ bool stamped(const Img &g, int p, uint8_t cur) { return (uint8_t)(g.mark[p] - cur) <= 1; }
+
+// stamp the 3x3 word neighbourhood of p for re-evaluation in the next pass
+// (byte stores; races benign since all writers store the same value)
+__device__ __forceinline__ void stamp3x3(const Img &g, int p, uint8_t v) {
+    uint8_t *m = g.mark + p;
+    const int S = g.S;
+    m[-S - 1] = v;
+    m[-S] = v;
+    m[-S + 1] = v;
+    m[-1] = v;
+    m[0] = v;
+    m[1] = v;
+    m[S - 1] = v;
+    m[S] = v;
+    m[S + 1] = v;
+}
+
+template <int FG>
+__device__ __forceinline__ uint32_t decide(uint32_t c, const Nb &i, const Nb &d, uint4 e0, uint4 e1) {
+    return c & simple_bits<FG>(i.nw ^ (d.nw & e0.x), i.n ^ (d.n & e0.y), i.ne ^ (d.ne & e0.z), i.w ^ (d.w & e0.w),
+                               i.e ^ (d.e & e1.x), i.sw ^ (d.sw & e1.y), i.s ^ (d.s & e1.z), i.se ^ (d.se & e1.w));
+}
+
+// ---- dense sweeps: strip walk with a sliding 3-row window ------------------
+struct Row3 {   // raw words x-1, x, x+1 of one row
+    uint32_t l, c, r;
+};
+__device__ __forceinline__ Row3 row3(const uint32_t *P, int p) { return Row3{P[p - 1], P[p], P[p + 1]}; }
+
+// one worklist pass over the strip; returns whether any decision changed.
+// Rows are processed in groups of kDenseBatch: the group's candidate / stamp
+// checks and E loads (from L2 when E does not fit in shared memory) are issued
+// together, then the rows are evaluated in order with the sliding window.
+constexpr int kDenseBatch = 4;
+
+template <int FG>
+__device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur, uint8_t next, int &evals) {
+    bool ch = false;
+    auto strip = [&](int x, int y0, int y1) {
+        if (y0 >= y1) return;
+        int p = pidx(g, y0, x);
+        Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
+        Row3 du = row3(g.D, p - g.S), dm = row3(g.D, p);
+        for (int yb = y0; yb < y1; yb += kDenseBatch) {
+            uint32_t cb[kDenseBatch];
+            uint4 e0b[kDenseBatch], e1b[kDenseBatch];
+#pragma unroll
+            for (int j = 0; j < kDenseBatch; ++j) {
+                const int q = p + j * g.S;
+                cb[j] = 0;
+                if (yb + j < y1) {
+                    const uint32_t c = g.C[q];
+                    if (c && (full || stamped(g, q, cur))) {
+                        cb[j] = c;
+                        const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
+                        e0b[j] = ep[0];
+                        e1b[j] = ep[1];
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kDenseBatch; ++j) {
+                if (yb + j >= y1) break;
+                const Row3 id = row3(g.I, p + g.S), dd = row3(g.D, p + g.S);
+                const uint32_t c = cb[j];
+                if (c) {
+                    Nb in, dn;
+                    in.nw = from_west(iu.l, iu.c);
+                    in.n = iu.c;
+                    in.ne = from_east(iu.c, iu.r);
+                    in.w = from_west(im.l, im.c);
+                    in.e = from_east(im.c, im.r);
+                    in.sw = from_west(id.l, id.c);
+                    in.s = id.c;
+                    in.se = from_east(id.c, id.r);
+                    dn.nw = from_west(du.l, du.c);
+                    dn.n = du.c;
+                    dn.ne = from_east(du.c, du.r);
+                    dn.w = from_west(dm.l, dm.c);
+                    dn.e = from_east(dm.c, dm.r);
+                    dn.sw = from_west(dd.l, dd.c);
+                    dn.s = dd.c;
+                    dn.se = from_east(dd.c, dd.r);
+                    const uint32_t nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
+                    ++evals;
+                    if (nd != dm.c) {
+                        g.D[p] = nd;
+                        dm.c = nd;   // the next row sees this update (Gauss-Seidel down the strip)
+                        stamp3x3(g, p, next);
+                        ch = true;
+                    }
+                }
+                iu = im;
+                im = id;
+                du = dm;
+                dm = dd;
+                p += g.S;
+            }
+        }
+    };
+    const int t = threadIdx.x;
+    if (g.WW <= kThreads) {
+        const int x = t % g.WW, blk = t / g.WW;
+        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb));
+    } else {
+        for (int x = t; x < g.WW; x += kThreads) strip(x, 0, g.H);
+    }
+    return ch;
+}
+
+// ---- sparse sweeps: list of words ------------------------------------------
+struct Slot {
+    int p;
+    Nb in;          // image neighbours at the sweep start
+    uint4 e0, e1;   // E masks
+    uint32_t c;     // candidates
+    uint32_t d;     // current decision (only this thread writes D[p])
+};
+
+template <int FG>
+__device__ __forceinline__ void load_slot(const Img &g, uint32_t p, Slot &s) {
+    s.p = (int)p;
+    s.in = nbrs(g.I, g, s.p);
+    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)s.p * 8);
+    s.e0 = ep[0];
+    s.e1 = ep[1];
+    s.c = g.C[s.p];
+    s.d = g.D[s.p];
+}
+
+template <int FG, bool STAMP>
+__device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t stamp = 0) {
+    const uint32_t *u = g.D + s.p - g.S, *m = g.D + s.p, *d = g.D + s.p + g.S;
+    Nb dn;
+    dn.nw = from_west(u[-1], u[0]);
+    dn.n = u[0];
+    dn.ne = from_east(u[0], u[1]);
+    dn.w = from_west(m[-1], s.d);   // W/E inside the word: own decisions
+    dn.e = from_east(s.d, m[1]);
+    dn.sw = from_west(d[-1], d[0]);
+    dn.s = d[0];
+    dn.se = from_east(d[0], d[1]);
+    const uint32_t nd = decide<FG>(s.c, s.in, dn, s.e0, s.e1);
+    if (nd != s.d) {
+        if constexpr (STAMP) stamp3x3(g, s.p, stamp);
+        s.d = nd;
+        g.D[s.p] = nd;
+        return true;
+    }
+    return false;
+}
+
+// mark the dirty bits of padded words [p0, p1] (consecutive, at most 3)
+__device__ __forceinline__ void mark_words(const Img &g, int p0, int p1) {
+    const int q0 = p0 >> 5, q1 = p1 >> 5;
+    if (q0 == q1) {
+        atomicOr(&g.dirty[q0], (0xFFFFFFFFu >> (31 - (p1 - p0))) << (p0 & 31));
+    } else {
+        atomicOr(&g.dirty[q0], 0xFFFFFFFFu << (p0 & 31));
+        atomicOr(&g.dirty[q1], 0xFFFFFFFFu >> (31 - (p1 & 31)));
+    }
+}
+
+// flips of one listed word: I ^= d, D = 0, dirty 3x3 word neighbourhood
+__device__ __forceinline__ unsigned apply_word(const Img &g, int p, uint32_t dw) {
+    if (!dw) return 0;
+    g.I[p] ^= dw;
+    g.D[p] = 0;
+    const int a = (dw & 1u) ? -1 : 0, b = (dw >> 31) ? 1 : 0;
+    mark_words(g, p - g.S + a, p - g.S + b);
+    mark_words(g, p + a, p + b);
+    mark_words(g, p + g.S + a, p + g.S + b);
+    return __popc(dw);
+}
+
+// re-examine every dirty word (warp per 32-word bitmap group, lane = word)
+template <int FG>
+__device__ __forceinline__ void rebuild_sparse(const Img &g, int t, int *counter) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nq = (g.plen + 31) >> 5;
+    for (int q = warp; q < nq; q += kWarps) {
+        const uint32_t bits = g.dirty[q];
+        if (bits == 0) continue;   // warp-uniform
+        __syncwarp();
+        if (lane == 0) g.dirty[q] = 0;
+        const int p = q * 32 + lane;
+        uint32_t c = 0;
+        if ((bits >> lane) & 1u) {
+            c = cand_word<FG>(g, p, t);
+            g.C[p] = c;
+            g.D[p] = c;
+        }
+        append(c != 0, (uint32_t)p, g.list, counter);
+    }
+}
+
+// recompute the candidates of every word (after a dense sweep)
+template <int FG>
+__device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter) {
+    for_strip(g, [&](int y, int x, int p) {
+        const uint32_t c = cand_word<FG>(g, p, t);
+        g.C[p] = c;
+        g.D[p] = c;
+        append(c != 0, (uint32_t)p, g.list, counter);
+    });
+}
+
+struct Stats {
+    long long sweeps, passes, calls;
+    long long cyc_prep, cyc_jacobi, cyc_update;   // thread-0 clock64 deltas (stats mode only)
+    long long cyc_tiny, n_tiny, pass_tiny;        // sweeps with <= 32 listed words
+    long long cyc_dense, n_dense, pass_dense;     // dense-mode sweeps
+    long long cyc_rank;                           // clamped-EDT part of prep
+    bool timing;
+};
+
+struct Shared {
+    int img;
+    int counters[2];
+    int bad;
+    unsigned long long flips, evals;
+};
+
+// ---- phase functions ----------------------------------------------------------
+// Each phase is a separate (non-inlined) function so that its register
+// allocation is independent of the others.  They receive the image as a View:
+// hot planes as 32-bit shared-window addresses (HOT) re-materialised with
+// cvta inside the callee (so accesses compile to LDS/STS), others as pointers.
+struct View {
+    unsigned long long I, D, C, B, dirty, mark;   // shared address (HOT) or pointer bits
+    uint32_t *list, *E, *XS, *R, *K, *A;
+    int H, W, WW, S, plen, org, nblk, hb, dense_min;
+    uint32_t lastmask;
+    uint32_t sh;   // shared address of the CTA's Shared block
+};
+
+template <bool HOT>
+__device__ __forceinline__ uint32_t *hot_ptr(unsigned long long h) {
+    if constexpr (HOT)
+        return reinterpret_cast<uint32_t *>(__cvta_shared_to_generic((size_t)h));
+    else
+        return reinterpret_cast<uint32_t *>(h);
+}
+
+template <bool HOT>
+__device__ __forceinline__ Img make_img(const View &v) {
+    Img g;
+    g.I = hot_ptr<HOT>(v.I);
+    g.D = hot_ptr<HOT>(v.D);
+    g.C = hot_ptr<HOT>(v.C);
+    g.B = hot_ptr<HOT>(v.B);
+    g.dirty = hot_ptr<HOT>(v.dirty);
+    g.mark = reinterpret_cast<uint8_t *>(hot_ptr<HOT>(v.mark));
+    g.list = v.list;
+    g.E = v.E;
+    g.XS = v.XS;
+    g.R = v.R;
+    g.K = v.K;
+    g.A = v.A;
+    g.H = v.H;
+    g.W = v.W;
+    g.WW = v.WW;
+    g.S = v.S;
+    g.plen = v.plen;
+    g.org = v.org;
+    g.nblk = v.nblk;
+    g.hb = v.hb;
+    g.dense_min = v.dense_min;
+    g.lastmask = v.lastmask;
+    return g;
+}
+
+__device__ __forceinline__ Shared *shared_block(const View &v) {
+    return reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh));
+}
+
+template <bool HOT, int R>
+__device__ __noinline__ int prep_nl(const View v, bool thin, int xmode, bool save_xs) {
+    const Img g = make_img<HOT>(v);
+    return prep_rank<R>(g, thin, xmode, save_xs);
+}
+
+template <bool HOT>
+__device__ __forceinline__ int prep_dispatch_v(int r, const View &v, bool thin, int xmode, bool save_xs) {
     switch (r) {
 #define TS_PREP_CASE(RR) \
     case RR:             \
-        return prep_rank<RR>(g, thin, xmode, save_xs);
+        return prep_nl<HOT, RR>(v, thin, xmode, save_xs);
         TS_PREP_CASE(1) TS_PREP_CASE(2) TS_PREP_CASE(3) TS_PREP_CASE(4)
         TS_PREP_CASE(5) TS_PREP_CASE(6) TS_PREP_CASE(7) TS_PREP_CASE(8)
         TS_PREP_CASE(9) TS_PREP_CASE(10) TS_PREP_CASE(11) TS_PREP_CASE(12)
@@ -313,358 +670,209 @@ __device__ __forceinline__ int prep_dispatch(int r, const Img &g, bool thin, int
             return -1;
     }
 }
-static_assert(kMaxR == 16, "prep_dispatch covers radii 1..16");
 
-__device__ __forceinline__ void cmp_step(uint32_t &lt, uint32_t &eq, uint32_t nb, uint32_t own) {
-    lt |= eq & ~nb & own;   // neighbour < own at the first differing slice
-    eq &= ~(nb ^ own);
+template <int FG, bool HOT, int S>
+__device__ __noinline__ void epass_nl(const View v, int t, int cur) {
+    const Img g = make_img<HOT>(v);
+    epass_ranks<FG, S>(g, t, &shared_block(v)->counters[cur]);
 }
 
-// E planes from rank slices + initial candidate list.  E_k(p) = key(q) < key(p)
-// for q = neighbour k, key = (rank, raster index) (topo.py:225,256): ties go to
-// the raster-earlier neighbours NW,N,NE,W.
-template <int FG>
-__device__ __forceinline__ void epass_ranks(const Img &g, int S, int t, int *counter) {
-    for (int base = 0; base < g.nwords; base += kThreads) {
-        const int w = base + threadIdx.x;
-        uint32_t c = 0, entry = 0;
-        if (w < g.nwords) {
-            int y, x;
-            word_yx(g, w, y, x);
-            const uint32_t bw = g.B[w];
-            if (~bw & valid_bits(g, x)) {
-                c = cand_word<FG>(g, y, x, t);
-                uint32_t lt[8], eq[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    lt[k] = 0;
-                    eq[k] = ~0u;
-                }
-                for (int s = S - 1; s >= 0; --s) {
-                    const uint32_t *P = g.R + (size_t)s * g.nwords;
-                    const Nb nb = nbrs(P, g, y, x);
-                    const uint32_t own = P[w];
-                    cmp_step(lt[0], eq[0], nb.nw, own);
-                    cmp_step(lt[1], eq[1], nb.n, own);
-                    cmp_step(lt[2], eq[2], nb.ne, own);
-                    cmp_step(lt[3], eq[3], nb.w, own);
-                    cmp_step(lt[4], eq[4], nb.e, own);
-                    cmp_step(lt[5], eq[5], nb.sw, own);
-                    cmp_step(lt[6], eq[6], nb.s, own);
-                    cmp_step(lt[7], eq[7], nb.se, own);
-                }
-                uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)w * 8);
-                ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
-                ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
-            }
-            g.D[w] = c;
-            entry = ((uint32_t)y << 16) | (uint32_t)x;
-        }
-        append(c != 0, entry, g.list, counter);
+template <int FG, bool HOT>
+__device__ __forceinline__ void epass_dispatch_v(const View &v, int S, int t, int cur) {
+    switch (S) {
+        case 1: epass_nl<FG, HOT, 1>(v, t, cur); break;
+        case 2: epass_nl<FG, HOT, 2>(v, t, cur); break;
+        case 3: epass_nl<FG, HOT, 3>(v, t, cur); break;
+        case 4: epass_nl<FG, HOT, 4>(v, t, cur); break;
+        case 5: epass_nl<FG, HOT, 5>(v, t, cur); break;
+        case 6: epass_nl<FG, HOT, 6>(v, t, cur); break;
+        default: epass_nl<FG, HOT, 7>(v, t, cur); break;
     }
 }
+static_assert(kMaxSlices <= 7, "epass_dispatch covers up to 7 rank slices");
 
-// E planes straight from an int64 priority map (public homotopic_thin /
-// homotopic_thicken: arbitrary priorities, topo.py:303-342)
-template <int FG>
-__device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, int t, int *counter) {
-    const int dy[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
-    const int dx[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
-    for (int base = 0; base < g.nwords; base += kThreads) {
-        const int w = base + threadIdx.x;
-        uint32_t c = 0, entry = 0;
-        if (w < g.nwords) {
-            int y, x;
-            word_yx(g, w, y, x);
-            const uint32_t bw = g.B[w];
-            if (~bw & valid_bits(g, x)) {
-                uint32_t e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                const int cnt = min(32, g.W - x * 32);
-                for (int i = 0; i < cnt; ++i) {
-                    const int col = x * 32 + i;
-                    const int64_t pv = prio[(size_t)y * g.W + col];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int ny = y + dy[k], nc = col + dx[k];
-                        if (ny < 0 || ny >= g.H || nc < 0 || nc >= g.W) continue;
-                        const int64_t q = prio[(size_t)ny * g.W + nc];
-                        if (q < pv || (q == pv && k < 4)) e[k] |= 1u << i;
-                    }
-                }
-                uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)w * 8);
-                ep[0] = make_uint4(e[0], e[1], e[2], e[3]);
-                ep[1] = make_uint4(e[4], e[5], e[6], e[7]);
-                c = cand_word<FG>(g, y, x, t);
-            }
-            g.D[w] = c;
-            entry = ((uint32_t)y << 16) | (uint32_t)x;
-        }
-        append(c != 0, entry, g.list, counter);
-    }
+template <int FG, bool HOT>
+__device__ __noinline__ void epass_prio_nl(const View v, const int64_t *prio, int t, int cur) {
+    const Img g = make_img<HOT>(v);
+    epass_prio<FG>(g, prio, t, &shared_block(v)->counters[cur]);
 }
 
-// sweep-constant data of one listed word: neighbour image words, precedence
-// masks and candidates (cached in registers for the thread's first slot)
-struct Slot {
-    int w, y, x;
-    bool up, dn, lf, rt;
-    Nb in;          // image neighbours at the sweep start
-    uint4 e0, e1;   // E masks
-    uint32_t c;     // candidates
-    uint32_t d;     // current decision (only this thread writes D[w])
+struct SweepOut {
+    long long passes;
+    unsigned flips;
+    int evals;
+    bool bad;
 };
 
-template <int FG>
-__device__ __forceinline__ void load_slot(const Img &g, uint32_t entry, Slot &s, int t) {
-    s.y = (int)(entry >> 16);
-    s.x = (int)(entry & 0xFFFFu);
-    s.w = s.y * g.WW + s.x;
-    s.up = s.y > 0;
-    s.dn = s.y + 1 < g.H;
-    s.lf = s.x > 0;
-    s.rt = s.x + 1 < g.WW;
-    s.in = nbrs(g.I, g, s.y, s.x);
-    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)s.w * 8);
-    s.e0 = ep[0];
-    s.e1 = ep[1];
-    // the sweep's candidates, recomputed from the sweep-start image
-    const uint32_t pre = valid_bits(g, s.x) & (t ? s.in.m : ~s.in.m) & ~g.B[s.w];
-    const Nb &i = s.in;
-    s.c = pre & simple_bits<FG>(i.nw, i.n, i.ne, i.w, i.e, i.sw, i.s, i.se);
-    s.d = g.D[s.w];
-}
-
-// position + current decision only (apply phase: must not read the image,
-// which other threads are updating)
-__device__ __forceinline__ void load_slot_pos(const Img &g, uint32_t entry, Slot &s) {
-    s.y = (int)(entry >> 16);
-    s.x = (int)(entry & 0xFFFFu);
-    s.w = s.y * g.WW + s.x;
-    s.up = s.y > 0;
-    s.dn = s.y + 1 < g.H;
-    s.lf = s.x > 0;
-    s.rt = s.x + 1 < g.WW;
-    s.d = g.D[s.w];
-}
-
-// stamp the word neighbourhood affected by changed decision bits `chg` of a
-// slot for re-evaluation in the next pass (byte stores, races benign)
-__device__ __forceinline__ void stamp_slot(const Img &g, const Slot &s, uint32_t chg, uint8_t v) {
-    const int xa = ((chg & 1u) && s.lf) ? s.x - 1 : s.x;
-    const int xb = ((chg >> 31) && s.rt) ? s.x + 1 : s.x;
-    const int ya = s.up ? s.y - 1 : s.y, yb = s.dn ? s.y + 1 : s.y;
-    for (int yy = ya; yy <= yb; ++yy)
-        for (int xx = xa; xx <= xb; ++xx) g.mark[yy * g.WW + xx] = v;
-}
-
-// one chaotic-fixpoint update of a slot's decisions; with STAMP, words whose
-// inputs changed are stamped for the next pass of the worklist
-template <int FG, bool STAMP>
-__device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t stamp = 0) {
-    const uint32_t *row = g.D + s.w;
-    const int WW = g.WW;
-    const uint32_t u1 = s.up ? row[-WW] : 0u, d1 = s.dn ? row[WW] : 0u;
-    const uint32_t u0 = (s.up && s.lf) ? row[-WW - 1] : 0u, u2 = (s.up && s.rt) ? row[-WW + 1] : 0u;
-    const uint32_t m0 = s.lf ? row[-1] : 0u, m2 = s.rt ? row[1] : 0u;
-    const uint32_t d0 = (s.dn && s.lf) ? row[WW - 1] : 0u, d2 = (s.dn && s.rt) ? row[WW + 1] : 0u;
-    const Nb d = shifts(u0, u1, u2, m0, s.d, m2, d0, d1, d2);   // W/E inside the word: own decisions
-    const Nb &i = s.in;
-    const uint32_t nd =
-        s.c & simple_bits<FG>(i.nw ^ (d.nw & s.e0.x), i.n ^ (d.n & s.e0.y), i.ne ^ (d.ne & s.e0.z),
-                              i.w ^ (d.w & s.e0.w), i.e ^ (d.e & s.e1.x), i.sw ^ (d.sw & s.e1.y),
-                              i.s ^ (d.s & s.e1.z), i.se ^ (d.se & s.e1.w));
-    if (nd != s.d) {
-        if constexpr (STAMP) stamp_slot(g, s, nd ^ s.d, stamp);
-        s.d = nd;
-        g.D[s.w] = nd;
-        return true;
-    }
-    return false;
-}
-
-// mark the bitmap bits of words [w0, w1] (consecutive, at most 3)
-__device__ __forceinline__ void mark_words(const Img &g, int w0, int w1) {
-    const int q0 = w0 >> 5, q1 = w1 >> 5;
-    if (q0 == q1) {
-        atomicOr(&g.dirty[q0], (0xFFFFFFFFu >> (31 - (w1 - w0))) << (w0 & 31));
-    } else {
-        atomicOr(&g.dirty[q0], 0xFFFFFFFFu << (w0 & 31));
-        atomicOr(&g.dirty[q1], 0xFFFFFFFFu >> (31 - (w1 & 31)));
-    }
-}
-
-// flips of one slot: I ^= d, D = 0, dirty 3x3 word neighbourhood
-__device__ __forceinline__ unsigned apply_slot(const Img &g, const Slot &s) {
-    const uint32_t dw = s.d;
-    if (!dw) return 0;
-    g.I[s.w] ^= dw;
-    g.D[s.w] = 0;
-    const int xa = ((dw & 1u) && s.lf) ? s.x - 1 : s.x;
-    const int xb = ((dw >> 31) && s.rt) ? s.x + 1 : s.x;
-    const int ya = s.up ? s.y - 1 : s.y, yb = s.dn ? s.y + 1 : s.y;
-    for (int yy = ya; yy <= yb; ++yy) mark_words(g, yy * g.WW + xa, yy * g.WW + xb);
-    return __popc(dw);
-}
-
-// re-examine every dirty word (warp per 32-word bitmap group, lane = word):
-// new candidates -> C, D (= tentative flip), list
-template <int FG>
-__device__ __forceinline__ void rebuild(const Img &g, int t, int *counter) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nq = (g.nwords + 31) >> 5;
-    for (int q = warp; q < nq; q += kWarps) {
-        const uint32_t bits = g.dirty[q];
-        if (bits == 0) continue;   // warp-uniform
-        __syncwarp();
-        if (lane == 0) g.dirty[q] = 0;
-        const int w = q * 32 + lane;
-        uint32_t c = 0, entry = 0;
-        if ((bits >> lane) & 1u) {
-            int y, x;
-            word_yx(g, w, y, x);
-            c = cand_word<FG>(g, y, x, t);
-            g.D[w] = c;
-            entry = ((uint32_t)y << 16) | (uint32_t)x;
+// dense sweep: worklist passes over the strips, then apply (all threads)
+template <int FG, bool HOT>
+__device__ __noinline__ SweepOut dense_sweep(const View v, long long cap, int pc0) {
+    const Img g = make_img<HOT>(v);
+    SweepOut o{0, 0, 0, false};
+    int pc = pc0;
+    while (true) {
+        const bool ch = dense_pass<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals);
+        ++o.passes;
+        ++pc;
+        if (!__syncthreads_or(ch)) break;
+        if (o.passes > cap) {
+            o.bad = true;
+            break;
         }
-        append(c != 0, entry, g.list, counter);
     }
+    for_strip(g, [&](int y, int x, int p) {
+        const uint32_t dw = g.D[p];
+        if (dw) {
+            g.I[p] ^= dw;
+            g.D[p] = 0;
+            o.flips += __popc(dw);
+        }
+    });
+    return o;
 }
 
-struct Stats {
-    long long sweeps, passes, calls;
-    long long cyc_prep, cyc_jacobi, cyc_update;   // thread-0 clock64 deltas (stats mode only)
-    long long cyc_tiny, n_tiny, pass_tiny;        // sweeps with <= 32 listed words
-    long long cyc_dense, n_dense, pass_dense;     // sweeps with > kThreads listed words
-    long long cyc_rank;                           // clamped-EDT part of prep
-    long long evals;                              // slot evaluations in worklist passes
-    bool timing;
-};
+// sparse sweep over the n listed words, then apply (all threads)
+template <int FG, bool HOT>
+__device__ __noinline__ SweepOut sparse_sweep(const View v, int n, long long cap, int pc0) {
+    const Img g = make_img<HOT>(v);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    SweepOut o{0, 0, 0, false};
+    int pc = pc0;
+    Slot s0;
+    const bool has0 = tid < n;
+    if (has0) load_slot<FG>(g, g.list[tid], s0);
+    if (n <= 32) {
+        // tiny sweep: one warp iterates to the fixpoint with warp syncs only
+        if (warp == 0) {
+            while (true) {
+                const bool ch = has0 && update_slot<FG, false>(g, s0);
+                ++o.passes;
+                __syncwarp();
+                if (!__any_sync(0xffffffffu, ch)) break;
+                if (o.passes > cap) {
+                    o.bad = true;
+                    break;
+                }
+            }
+            if (has0) o.flips += apply_word(g, s0.p, s0.d);
+        }
+        return o;
+    }
+    while (true) {
+        const uint8_t cur_stamp = (uint8_t)pc, next_stamp = (uint8_t)(pc + 1);
+        const bool full = o.passes == 0;
+        bool ch = false;
+        if (has0 && (full || stamped(g, s0.p, cur_stamp))) {
+            ch = update_slot<FG, true>(g, s0, next_stamp);
+            ++o.evals;
+        }
+        for (int sl = tid + kThreads; sl < n; sl += kThreads) {
+            const uint32_t p = g.list[sl];
+            if (!full && !stamped(g, (int)p, cur_stamp)) continue;
+            Slot s;
+            load_slot<FG>(g, p, s);
+            ch |= update_slot<FG, true>(g, s, next_stamp);
+            ++o.evals;
+        }
+        ++o.passes;
+        ++pc;
+        if (!__syncthreads_or(ch)) break;
+        if (o.passes > cap) {
+            o.bad = true;
+            break;
+        }
+    }
+    if (has0) o.flips += apply_word(g, s0.p, s0.d);
+    for (int sl = tid + kThreads; sl < n; sl += kThreads) {
+        const int p = (int)g.list[sl];
+        o.flips += apply_word(g, p, g.D[p]);
+    }
+    return o;
+}
+
+template <int FG, bool HOT>
+__device__ __noinline__ void rebuild_nl(const View v, bool dense, int t, int cur) {
+    const Img g = make_img<HOT>(v);
+    int *counter = &shared_block(v)->counters[cur];
+    if (dense)
+        rebuild_dense<FG>(g, t, counter);
+    else
+        rebuild_sparse<FG>(g, t, counter);
+}
+
+// discard a prepared sweep (max_iter reached): D and C back to zero
+template <bool HOT>
+__device__ __noinline__ void discard_nl(const View v, int n) {
+    const Img g = make_img<HOT>(v);
+    for (int s = threadIdx.x; s < n; s += kThreads) {
+        const int p = (int)g.list[s];
+        g.D[p] = 0;
+        g.C[p] = 0;
+    }
+}
 
 // the priority-ordered flip engine (topo.py:211-258), see file header.
-// Precondition (after a __syncthreads): list/C/D built, counters[cur] = size,
-// dirty all zero, D zero outside listed words.
-template <int FG>
-__device__ __forceinline__ void engine(const Img &g, int t, long long max_sweeps, int *counters, int &cur, int *err,
-                                       Stats &st, unsigned long long *s_flips, int *s_bad, int &pc,
-                                       unsigned long long *s_evals) {
-    const int tid = threadIdx.x, warp = tid >> 5;
+// Precondition (after a __syncthreads): C = candidates of every word, D = C,
+// list = words with C != 0, counters[cur] = its size, dirty bitmap zero.
+template <int FG, bool HOT>
+__device__ __forceinline__ void engine(const View &v, int t, long long max_sweeps, Shared &sh, int &cur, int *err,
+                                       Stats &st, int &pc) {
+    const int tid = threadIdx.x;
     long long sweeps = 0;
-    const long long sweep_cap = (long long)g.H * g.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
+    const long long sweep_cap = (long long)v.H * v.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
     while (true) {
-        const int n = counters[cur];
+        const int n = sh.counters[cur];
         if (n == 0) break;
         if ((max_sweeps >= 0 && sweeps >= max_sweeps) || sweeps >= sweep_cap) {
             if (sweeps >= sweep_cap && (max_sweeps < 0 || sweeps < max_sweeps)) {
                 if (tid == 0) set_err(err, ERR_SWEEP_CAP);
             }
-            for (int s = tid; s < n; s += kThreads) {
-                const uint32_t e = g.list[s];
-                g.D[(int)(e >> 16) * g.WW + (int)(e & 0xFFFFu)] = 0;
-            }
+            discard_nl<HOT>(v, n);
             __syncthreads();
             break;
         }
         const long long tj0 = st.timing ? clock64() : 0;
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
-        long long passes = 0;
-        unsigned flips = 0;
-        Slot s0;
-        const bool has0 = tid < n;
-        if (has0) load_slot<FG>(g, g.list[tid], s0, t);
-        if (n <= 32) {
-            // tiny sweep: one warp iterates to the fixpoint with warp syncs only
-            if (warp == 0) {
-                bool bad = false;
-                while (true) {
-                    const bool ch = has0 && update_slot<FG, false>(g, s0);
-                    ++passes;
-                    __syncwarp();
-                    if (!__any_sync(0xffffffffu, ch)) break;
-                    if (passes > cap) {
-                        bad = true;
-                        break;
-                    }
-                }
-                if (tid == 0) {
-                    *s_bad = bad ? 1 : 0;
-                    counters[cur ^ 1] = 0;
-                }
-                if (has0) flips += apply_slot(g, s0);
-            }
-            __syncthreads();
-        } else {
-            // worklist passes: pass 1 evaluates every slot; later passes only the
-            // words stamped (by a changed neighbour decision) with the current
-            // pass number.  A pass without change is a fixpoint: every slot was
-            // last evaluated after its last input change.
-            bool bad = false;
-            while (true) {
-                const uint8_t cur_stamp = (uint8_t)pc, next_stamp = (uint8_t)(pc + 1);
-                const bool full = passes == 0;
-                bool ch = false;
-                int ev = 0;
-                if (has0 && (full || (uint8_t)(g.mark[s0.w] - cur_stamp) <= 1)) {
-                    ch = update_slot<FG, true>(g, s0, next_stamp);
-                    ++ev;
-                }
-                for (int sl = tid + kThreads; sl < n; sl += kThreads) {
-                    const uint32_t e = g.list[sl];
-                    if (!full) {
-                        const int w = (int)(e >> 16) * g.WW + (int)(e & 0xFFFFu);
-                        if ((uint8_t)(g.mark[w] - cur_stamp) > 1) continue;
-                    }
-                    Slot s;
-                    load_slot<FG>(g, e, s, t);
-                    ch |= update_slot<FG, true>(g, s, next_stamp);
-                    ++ev;
-                }
-                if (st.timing) {
-                    ev = __reduce_add_sync(0xffffffffu, ev);
-                    if ((tid & 31) == 0 && ev) atomicAdd(s_evals, (unsigned long long)ev);
-                }
-                ++passes;
-                ++pc;
-                if (!__syncthreads_or(ch)) break;
-                if (passes > cap) {
-                    bad = true;
-                    break;
-                }
-            }
-            if (tid == 0) {
-                *s_bad = bad ? 1 : 0;
-                counters[cur ^ 1] = 0;
-            }
-            if (has0) flips += apply_slot(g, s0);
-            for (int sl = tid + kThreads; sl < n; sl += kThreads) {
-                Slot s;
-                load_slot_pos(g, g.list[sl], s);
-                flips += apply_slot(g, s);
-            }
-            __syncthreads();
+        const bool dense = n > v.dense_min;
+        const SweepOut o = dense ? dense_sweep<FG, HOT>(v, cap, pc) : sparse_sweep<FG, HOT>(v, n, cap, pc);
+        if (tid == 0) {
+            sh.bad = o.bad ? 1 : 0;
+            sh.counters[cur ^ 1] = 0;
         }
-        if (*s_bad) {
+        __syncthreads();
+        if (sh.bad) {
             if (tid == 0) set_err(err, ERR_JACOBI_CAP);
             break;
         }
-        if (s_flips && flips) atomicAdd(s_flips, (unsigned long long)flips);
+        // pass counter must stay block-uniform: tiny sweeps (one warp, no stamps)
+        // do not advance it; dense and list sweeps count passes uniformly
+        if (dense || n > 32) pc += (int)o.passes;
+        if (st.timing) {
+            const int ev = __reduce_add_sync(0xffffffffu, o.evals);
+            const unsigned fl = __reduce_add_sync(0xffffffffu, o.flips);
+            if ((tid & 31) == 0) {
+                if (ev) atomicAdd(&sh.evals, (unsigned long long)ev);
+                if (fl) atomicAdd(&sh.flips, (unsigned long long)fl);
+            }
+        }
         const long long tj1 = st.timing ? clock64() : 0;
         cur ^= 1;
-        rebuild<FG>(g, t, &counters[cur]);
+        rebuild_nl<FG, HOT>(v, dense, t, cur);
         __syncthreads();
         ++sweeps;
-        st.passes += passes;
+        st.passes += o.passes;
         if (st.timing) {
             const long long tj2 = clock64();
             st.cyc_jacobi += tj1 - tj0;
             st.cyc_update += tj2 - tj1;
-            if (n <= 32) {
-                st.cyc_tiny += tj1 - tj0;
-                st.n_tiny += 1;
-                st.pass_tiny += passes;
-            } else if (n > kThreads) {
+            if (dense) {
                 st.cyc_dense += tj1 - tj0;
                 st.n_dense += 1;
-                st.pass_dense += passes;
+                st.pass_dense += o.passes;
+            } else if (n <= 32) {
+                st.cyc_tiny += tj1 - tj0;
+                st.n_tiny += 1;
+                st.pass_tiny += o.passes;
             }
         }
     }
@@ -672,101 +880,124 @@ __device__ __forceinline__ void engine(const Img &g, int t, long long max_sweeps
     st.calls += 1;
 }
 
-template <int FG>
-__device__ __forceinline__ void run_stage(const Img &g, int r, bool thin, int xmode, bool save_xs, int *counters,
-                                          int &cur, int *err, Stats &st, unsigned long long *s_flips, int *s_bad,
-                                          int &pc, unsigned long long *s_evals) {
-    if (threadIdx.x == 0) counters[cur] = 0;
+template <int FG, bool HOT>
+__device__ __forceinline__ void run_stage(const View &v, int r, bool thin, int xmode, bool save_xs, Shared &sh,
+                                          int &cur, int *err, Stats &st, int &pc) {
+    if (threadIdx.x == 0) sh.counters[cur] = 0;
     const long long tp0 = st.timing ? clock64() : 0;
-    const int S = prep_dispatch(r, g, thin, xmode, save_xs);
+    const int S = prep_dispatch_v<HOT>(r, v, thin, xmode, save_xs);
     __syncthreads();
     if (st.timing) st.cyc_rank += clock64() - tp0;
-    epass_ranks<FG>(g, S, thin ? 1 : 0, &counters[cur]);
+    epass_dispatch_v<FG, HOT>(v, S, thin ? 1 : 0, cur);
     __syncthreads();
     if (st.timing) st.cyc_prep += clock64() - tp0;
-    engine<FG>(g, thin ? 1 : 0, -1, counters, cur, err, st, s_flips, s_bad, pc, s_evals);
+    engine<FG, HOT>(v, thin ? 1 : 0, -1, sh, cur, err, st, pc);
+}
+
+// image prologue: clear planes, pack inputs, validate (all threads)
+template <bool HOT>
+__device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size_t pix) {
+    const KParams &p = *pp;
+    const Img g = make_img<HOT>(v);
+    const int tid = threadIdx.x;
+    const bool has_k = p.keep != nullptr, has_a = p.avoid != nullptr;
+    for (int q = tid; q < g.plen; q += kThreads) {
+        g.I[q] = 0;
+        g.D[q] = 0;
+        g.C[q] = 0;
+        g.B[q] = ~0u;   // pads blocked
+    }
+    for (int q = tid; q < (g.plen + 31) >> 5; q += kThreads) g.dirty[q] = 0;
+    for (int q = tid; q < (g.plen + 15) >> 4; q += kThreads)
+        reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
+    if (p.mode == MODE_THIN || p.mode == MODE_THICKEN) {
+        pack_plane(p.keep + pix, g.B, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+    } else {
+        if (has_k) pack_plane(p.keep + pix, g.K, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+        if (has_a) pack_plane(p.avoid + pix, g.A, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+    }
+    __syncthreads();
+    for_strip(g, [&](int y, int x, int q) {
+        const uint32_t X = g.I[q];
+        if (p.mode == MODE_THIN) {
+            if (g.B[q] & ~X) set_err(p.err, ERR_KEEP_NOT_OBJECT);          // topo.py:264-265
+        } else if (p.mode == MODE_THICKEN) {
+            const uint32_t allowed = g.B[q];
+            if (X & ~allowed) set_err(p.err, ERR_ALLOWED_NOT_SUPERSET);    // topo.py:332-333
+            g.B[q] = ~allowed;   // blocked = not allowed; padding bits blocked
+        } else {
+            const uint32_t K = has_k ? g.K[q] : 0u, A = has_a ? g.A[q] : 0u;
+            if (K & A) set_err(p.err, ERR_KEEP_AVOID);                     // smoothing.py:201-202
+            if (K & ~X) set_err(p.err, ERR_KEEP_NOT_OBJECT);               // smoothing.py:203-204
+            if (A & X) set_err(p.err, ERR_AVOID_ON_OBJECT);                // smoothing.py:205-206
+        }
+    });
+}
+
+template <bool HOT>
+__device__ __noinline__ void store_image_nl(const View v, uint8_t *out) {
+    const Img g = make_img<HOT>(v);
+    unpack_plane(g.I, out, g);
 }
 
 template <int FG, bool HOT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ int s_img;
-    __shared__ int s_counters[2];
-    __shared__ int s_bad;
-    __shared__ unsigned long long s_flips;
-    __shared__ unsigned long long s_evals;
+    __shared__ Shared sh;
 
     uint32_t *cta = p.gws + (size_t)blockIdx.x * (size_t)p.gws_stride;
     auto buf = [&](int b) -> uint32_t * { return ((p.smem_mask >> b) & 1u) ? smem + p.off[b] : cta + p.off[b]; };
-    Img g;
-    if constexpr (HOT) {   // derived from the shared array: compiled to LDS/STS
-        g.I = smem + p.off[B_I];
-        g.D = smem + p.off[B_D];
-        g.B = smem + p.off[B_B];
-        g.dirty = smem + p.off[B_DIRTY];
-        g.mark = reinterpret_cast<uint8_t *>(smem + p.off[B_MARK]);
+    View v;
+    if constexpr (HOT) {
+        const unsigned long long base = (unsigned long long)__cvta_generic_to_shared(smem);
+        v.I = base + 4ull * p.off[B_I];
+        v.D = base + 4ull * p.off[B_D];
+        v.C = base + 4ull * p.off[B_C];
+        v.B = base + 4ull * p.off[B_B];
+        v.dirty = base + 4ull * p.off[B_DIRTY];
+        v.mark = base + 4ull * p.off[B_MARK];
     } else {
-        g.I = buf(B_I);
-        g.D = buf(B_D);
-        g.B = buf(B_B);
-        g.dirty = buf(B_DIRTY);
-        g.mark = reinterpret_cast<uint8_t *>(buf(B_MARK));
+        v.I = (unsigned long long)buf(B_I);
+        v.D = (unsigned long long)buf(B_D);
+        v.C = (unsigned long long)buf(B_C);
+        v.B = (unsigned long long)buf(B_B);
+        v.dirty = (unsigned long long)buf(B_DIRTY);
+        v.mark = (unsigned long long)buf(B_MARK);
     }
-    g.list = buf(B_LIST);
-    g.E = buf(B_E);
-    g.XS = buf(B_XS);
-    g.R = buf(B_R);
-    g.K = buf(B_K);
-    g.A = buf(B_A);
-    g.H = p.H;
-    g.W = p.W;
-    g.WW = p.WW;
-    g.nwords = p.nwords;
-    g.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
-    g.ww_shift = (p.WW & (p.WW - 1)) == 0 ? __ffs(p.WW) - 1 : -1;
+    v.list = buf(B_LIST);
+    v.E = buf(B_E);
+    v.XS = buf(B_XS);
+    v.R = buf(B_R);
+    v.K = buf(B_K);
+    v.A = buf(B_A);
+    v.H = p.H;
+    v.W = p.W;
+    v.WW = p.WW;
+    v.S = p.stride;
+    v.plen = p.plen;
+    v.org = kPadRows * p.stride + 1;
+    v.nblk = p.nblk;
+    v.hb = p.hb;
+    v.dense_min = p.dense_min;
+    v.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
+    v.sh = (uint32_t)__cvta_generic_to_shared(&sh);
     const bool has_k = p.keep != nullptr, has_a = p.avoid != nullptr;
-    const int nq = (g.nwords + 31) >> 5;
+    const int tid = threadIdx.x;
 
     for (;;) {
-        if (threadIdx.x == 0) s_img = atomicAdd(p.counter, 1);
+        if (tid == 0) sh.img = atomicAdd(p.counter, 1);
         __syncthreads();
-        const int img = s_img;
+        const int img = sh.img;
         if (img >= p.n) break;
         const size_t pix = (size_t)img * p.H * p.W;
-
-        // ---- load + validate -------------------------------------------------
-        pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
-        if (p.mode == MODE_THIN || p.mode == MODE_THICKEN) {
-            pack_plane(p.keep + pix, g.B, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
-        } else {
-            if (has_k) pack_plane(p.keep + pix, g.K, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
-            if (has_a) pack_plane(p.avoid + pix, g.A, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+        if (tid == 0) {
+            sh.counters[0] = 0;
+            sh.flips = 0;
+            sh.evals = 0;
         }
-        for (int w = threadIdx.x; w < g.nwords; w += kThreads) g.D[w] = 0;
-        for (int q = threadIdx.x; q < nq; q += kThreads) g.dirty[q] = 0;
-        for (int q = threadIdx.x; q < (g.nwords + 15) >> 4; q += kThreads)
-            reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x == 0) {
-            s_counters[0] = 0;
-            s_flips = 0;
-            s_evals = 0;
-        }
-        __syncthreads();
-        for (int w = threadIdx.x; w < g.nwords; w += kThreads) {
-            const uint32_t X = g.I[w];
-            if (p.mode == MODE_THIN) {
-                if (g.B[w] & ~X) set_err(p.err, ERR_KEEP_NOT_OBJECT);          // topo.py:264-265
-            } else if (p.mode == MODE_THICKEN) {
-                const uint32_t allowed = g.B[w];
-                if (X & ~allowed) set_err(p.err, ERR_ALLOWED_NOT_SUPERSET);    // topo.py:332-333
-                g.B[w] = ~allowed;   // blocked = not allowed; padding bits blocked
-            } else {
-                const uint32_t K = has_k ? g.K[w] : 0u, A = has_a ? g.A[w] : 0u;
-                if (K & A) set_err(p.err, ERR_KEEP_AVOID);                     // smoothing.py:201-202
-                if (K & ~X) set_err(p.err, ERR_KEEP_NOT_OBJECT);               // smoothing.py:203-204
-                if (A & X) set_err(p.err, ERR_AVOID_ON_OBJECT);                // smoothing.py:205-206
-            }
-        }
+        load_image_nl<HOT>(v, &p, pix);
         __syncthreads();
 
         Stats st{};
@@ -774,7 +1005,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         const long long t_img0 = st.timing ? clock64() : 0;
         int cur = 0;
         int pc = 2;   // worklist pass counter (stamps are its low byte; marks start at 0)
-        unsigned long long *fl = p.stats ? &s_flips : nullptr;
         if (p.mode == MODE_HASF) {
             // stage table: (thin, xmode, save_xs) for S1/S3 (cutting) and S5/S7 (filling)
             const int first = p.do_cut ? 0 : 2, last = p.do_fill ? 3 : 1;
@@ -783,23 +1013,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
                     const bool thin = stg == 0 || stg == 3;
                     const int xmode = (stg == 1 || stg == 3) ? 2 : ((stg == 0 ? has_k : has_a) ? 1 : 0);
                     const bool save = stg == 0 || stg == 2;
-                    run_stage<FG>(g, r, thin, xmode, save, s_counters, cur, p.err, st, fl, &s_bad, pc, &s_evals);
+                    run_stage<FG, HOT>(v, r, thin, xmode, save, sh, cur, p.err, st, pc);
                 }
             }
         } else {
             const int t = p.mode == MODE_THIN ? 1 : 0;
-            epass_prio<FG>(g, p.prio + pix, t, &s_counters[cur]);
+            epass_prio_nl<FG, HOT>(v, p.prio + pix, t, cur);
             __syncthreads();
-            engine<FG>(g, t, p.max_sweeps, s_counters, cur, p.err, st, fl, &s_bad, pc, &s_evals);
+            engine<FG, HOT>(v, t, p.max_sweeps, sh, cur, p.err, st, pc);
         }
 
-        unpack_plane(g.I, p.out + pix, g);
-        if (threadIdx.x == 0 && p.stats) {
+        store_image_nl<HOT>(v, p.out + pix);
+        if (tid == 0 && p.stats) {
             long long *sp = p.stats + (size_t)img * kStatFields;
             sp[0] = st.sweeps;
             sp[1] = st.passes;
             sp[2] = st.calls;
-            sp[3] = (long long)s_flips;
+            sp[3] = (long long)sh.flips;
             sp[4] = st.cyc_prep;
             sp[5] = st.cyc_jacobi;
             sp[6] = st.cyc_update;
@@ -811,26 +1041,26 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sp[12] = st.n_dense;
             sp[13] = st.pass_dense;
             sp[14] = st.cyc_rank;
-            sp[15] = (long long)s_evals;
+            sp[15] = (long long)sh.evals;
         }
         __syncthreads();
     }
 }
 
 // per-variant host entry points, one translation unit each (ts_hasf_<fg><h|g>.cu)
-#define TS_DEFINE_HASF_VARIANT(FG, HOT, SUFFIX)                                                              \
-    cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream) {    \
-        const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                  \
+#define TS_DEFINE_HASF_VARIANT(FG, HOT, SUFFIX)                                                                \
+    cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream) {      \
+        const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
-        if (e != cudaSuccess) return e;                                                                       \
-        void *args[] = {(void *)&p};                                                                          \
-        return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);                   \
-    }                                                                                                         \
-    cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks) {                                     \
-        const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                  \
+        if (e != cudaSuccess) return e;                                                                         \
+        void *args[] = {(void *)&p};                                                                            \
+        return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);                     \
+    }                                                                                                           \
+    cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks) {                                       \
+        const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
-        if (e != cudaSuccess) return e;                                                                       \
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, kThreads, smem_bytes);              \
+        if (e != cudaSuccess) return e;                                                                         \
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, kThreads, smem_bytes);                \
     }
 
 }  // namespace ts

@@ -7,18 +7,24 @@ namespace ts {
 // Per-image working buffers of the fused HASF kernel.  Each lives either in
 // the CTA's shared memory or in its private slice of a global workspace
 // (L2-resident); the host places them greedily in this priority order.
+// All planes use the padded layout: kPadRows zero rows above and below the
+// image, one zero word between rows (row stride `stride` >= WW + 1); word
+// (y, x) is at (kPadRows + y) * stride + x + 1; plane length `plen` words.
+constexpr int kPadRows = 16;
+
 enum Buf : int {
-    B_I = 0,     // current image, bit-packed                          nwords
-    B_D,         // fixpoint decisions of the current sweep            nwords
-    B_B,         // blocked (floor) plane                              nwords
-    B_DIRTY,     // "re-examine" bitmap, 1 bit per word                ceil(nwords/32)
-    B_MARK,      // per-word pass stamps of the fixpoint worklist      nwords bytes
-    B_LIST,      // active-word list, (y << 16) | x                    nwords
-    B_E,         // 8 "earlier neighbour" masks per word, interleaved  8 * nwords
-    B_XS,        // saved image (cutting input X / filling input X')   nwords
-    B_R,         // rank bit-slices of the clamped distance map        S * nwords
-    B_K,         // keep constraint plane (optional)                   nwords
-    B_A,         // avoid constraint plane (optional)                  nwords
+    B_I = 0,     // current image, bit-packed                          plen
+    B_D,         // fixpoint decisions of the current sweep            plen
+    B_C,         // candidates of the current sweep                    plen
+    B_B,         // blocked (floor) plane; pads blocked                plen
+    B_DIRTY,     // "re-examine" bitmap, 1 bit per word                plen / 32
+    B_MARK,      // per-word pass stamps of the fixpoint worklist      plen bytes
+    B_LIST,      // active-word list (padded word indices)             plen
+    B_E,         // 8 "earlier neighbour" masks per word, interleaved  8 * plen
+    B_XS,        // saved image (cutting input X / filling input X')   plen
+    B_R,         // rank bit-slices of the clamped distance map        S * plen
+    B_K,         // keep constraint plane (optional)                   plen
+    B_A,         // avoid constraint plane (optional)                  plen
     B_COUNT
 };
 
@@ -50,6 +56,9 @@ struct KParams {
     const uint8_t *avoid;   // [n,h,w] or null
     const int64_t *prio;    // [n,h,w] (engine modes only)
     int n, H, W, WW, nwords;
+    int stride, plen;       // padded layout (see kPadRows)
+    int nblk, hb;           // strip mapping: row blocks per word column, rows per block
+    int dense_min;          // sweeps with more listed words run in dense (strip) mode
     int r_first, r_last, do_cut, do_fill;
     int mode;
     long long max_sweeps;   // < 0: unbounded
@@ -57,7 +66,7 @@ struct KParams {
     uint32_t *gws;          // global workspace, gws_stride words per CTA
     long long gws_stride;
     uint32_t smem_mask;     // bit b set: buffer b lives in shared memory
-    int hot;                // I, D, B, DIRTY, MARK all in shared memory (fast variant)
+    int hot;                // I, D, C, B, DIRTY, MARK all in shared memory (fast variant)
     long long off[B_COUNT]; // word offset of each buffer (smem or CTA slice)
     int *counter;           // image queue head
     int *err;               // first error code (atomicCAS from 0)
