@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <climits>
 #include <cstdint>
 #include <cstring>
@@ -156,9 +157,27 @@ void plan_strips(int H, int WW, int threads, Plan &pl) {
     pl.stride = best_s;
 }
 
+// Keep freed workspace in the device's stream-ordered pool across calls (the
+// default release threshold of 0 returns it to the OS at every synchronize,
+// which re-maps tens of MB per call).  Once per device.
+std::mutex g_pool_mu;
+bool g_pool_done[64] = {};
+
+void retain_pool(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64 || g_pool_done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    g_pool_done[dev] = true;
+}
+
 int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
     int dev = 0;
     TS_CUDA(cudaGetDevice(&dev));
+    retain_pool(dev);
     TS_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
     TS_CUDA(cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     TS_CUDA(cudaDeviceGetAttribute(smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));

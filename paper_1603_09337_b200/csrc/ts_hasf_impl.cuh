@@ -705,9 +705,8 @@ struct SweepOut {
 };
 
 // dense sweep: worklist passes over the strips, then apply (all threads)
-template <int FG, bool HOT>
-__device__ __noinline__ SweepOut dense_sweep(const View v, long long cap, int pc0) {
-    const Img g = make_img<HOT>(v);
+template <int FG>
+__device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int pc0) {
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
     while (true) {
@@ -732,9 +731,8 @@ __device__ __noinline__ SweepOut dense_sweep(const View v, long long cap, int pc
 }
 
 // sparse sweep over the n listed words, then apply (all threads)
-template <int FG, bool HOT>
-__device__ __noinline__ SweepOut sparse_sweep(const View v, int n, long long cap, int pc0) {
-    const Img g = make_img<HOT>(v);
+template <int FG>
+__device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long cap, int pc0) {
     const int tid = threadIdx.x, warp = tid >> 5;
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
@@ -790,10 +788,8 @@ __device__ __noinline__ SweepOut sparse_sweep(const View v, int n, long long cap
     return o;
 }
 
-template <int FG, bool HOT>
-__device__ __noinline__ void rebuild_nl(const View v, bool dense, int t, int cur) {
-    const Img g = make_img<HOT>(v);
-    int *counter = &shared_block(v)->counters[cur];
+template <int FG>
+__device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int t, int *counter) {
     if (dense)
         rebuild_dense<FG>(g, t, counter);
     else
@@ -801,9 +797,7 @@ __device__ __noinline__ void rebuild_nl(const View v, bool dense, int t, int cur
 }
 
 // discard a prepared sweep (max_iter reached): D and C back to zero
-template <bool HOT>
-__device__ __noinline__ void discard_nl(const View v, int n) {
-    const Img g = make_img<HOT>(v);
+__device__ __forceinline__ void discard_sweep(const Img &g, int n) {
     for (int s = threadIdx.x; s < n; s += kThreads) {
         const int p = (int)g.list[s];
         g.D[p] = 0;
@@ -814,12 +808,23 @@ __device__ __noinline__ void discard_nl(const View v, int n) {
 // the priority-ordered flip engine (topo.py:211-258), see file header.
 // Precondition (after a __syncthreads): C = candidates of every word, D = C,
 // list = words with C != 0, counters[cur] = its size, dirty bitmap zero.
+struct EngineIO {   // engine state carried across calls (block-uniform)
+    int cur, pc;
+    long long sweeps, passes, calls;
+    long long cyc_jacobi, cyc_update, cyc_tiny, n_tiny, pass_tiny, cyc_dense, n_dense, pass_dense;
+};
+
 template <int FG, bool HOT>
-__device__ __forceinline__ void engine(const View &v, int t, long long max_sweeps, Shared &sh, int &cur, int *err,
-                                       Stats &st, int &pc) {
+__device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sweeps, int *err, bool timing,
+                                           EngineIO io) {
+    const Img g = make_img<HOT>(v);
+    Shared &sh = *shared_block(v);
     const int tid = threadIdx.x;
+    int cur = io.cur, pc = io.pc;
+    Stats st{};
+    st.timing = timing;
     long long sweeps = 0;
-    const long long sweep_cap = (long long)v.H * v.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
+    const long long sweep_cap = (long long)g.H * g.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
     while (true) {
         const int n = sh.counters[cur];
         if (n == 0) break;
@@ -827,14 +832,18 @@ __device__ __forceinline__ void engine(const View &v, int t, long long max_sweep
             if (sweeps >= sweep_cap && (max_sweeps < 0 || sweeps < max_sweeps)) {
                 if (tid == 0) set_err(err, ERR_SWEEP_CAP);
             }
-            discard_nl<HOT>(v, n);
+            discard_sweep(g, n);
             __syncthreads();
             break;
         }
         const long long tj0 = st.timing ? clock64() : 0;
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
-        const bool dense = n > v.dense_min;
-        const SweepOut o = dense ? dense_sweep<FG, HOT>(v, cap, pc) : sparse_sweep<FG, HOT>(v, n, cap, pc);
+        const bool dense = n > g.dense_min;
+        SweepOut o;
+        if (dense)
+            o = dense_sweep<FG>(g, cap, pc);
+        else
+            o = sparse_sweep<FG>(g, n, cap, pc);
         if (tid == 0) {
             sh.bad = o.bad ? 1 : 0;
             sh.counters[cur ^ 1] = 0;
@@ -857,7 +866,7 @@ __device__ __forceinline__ void engine(const View &v, int t, long long max_sweep
         }
         const long long tj1 = st.timing ? clock64() : 0;
         cur ^= 1;
-        rebuild_nl<FG, HOT>(v, dense, t, cur);
+        rebuild_any<FG>(g, dense, t, &sh.counters[cur]);
         __syncthreads();
         ++sweeps;
         st.passes += o.passes;
@@ -876,8 +885,42 @@ __device__ __forceinline__ void engine(const View &v, int t, long long max_sweep
             }
         }
     }
-    st.sweeps += sweeps;
-    st.calls += 1;
+    io.cur = cur;
+    io.pc = pc;
+    io.sweeps += sweeps;
+    io.passes += st.passes;
+    io.calls += 1;
+    io.cyc_jacobi += st.cyc_jacobi;
+    io.cyc_update += st.cyc_update;
+    io.cyc_tiny += st.cyc_tiny;
+    io.n_tiny += st.n_tiny;
+    io.pass_tiny += st.pass_tiny;
+    io.cyc_dense += st.cyc_dense;
+    io.n_dense += st.n_dense;
+    io.pass_dense += st.pass_dense;
+    return io;
+}
+
+template <int FG, bool HOT>
+__device__ __forceinline__ void engine(const View &v, int t, long long max_sweeps, Shared &sh, int &cur, int *err,
+                                       Stats &st, int &pc) {
+    EngineIO io{};
+    io.cur = cur;
+    io.pc = pc;
+    io = engine_nl<FG, HOT>(v, t, max_sweeps, err, st.timing, io);
+    cur = io.cur;
+    pc = io.pc;
+    st.sweeps += io.sweeps;
+    st.passes += io.passes;
+    st.calls += io.calls;
+    st.cyc_jacobi += io.cyc_jacobi;
+    st.cyc_update += io.cyc_update;
+    st.cyc_tiny += io.cyc_tiny;
+    st.n_tiny += io.n_tiny;
+    st.pass_tiny += io.pass_tiny;
+    st.cyc_dense += io.cyc_dense;
+    st.n_dense += io.n_dense;
+    st.pass_dense += io.pass_dense;
 }
 
 template <int FG, bool HOT>
