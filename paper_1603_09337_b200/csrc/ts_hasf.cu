@@ -5,7 +5,6 @@
 
 namespace ts {
 
-constexpr int kThreadsHost = 512;
 
 #define TS_DECLARE_HASF_VARIANT(SUFFIX)                                                                   \
     cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream); \
@@ -25,6 +24,6 @@ cudaError_t hasf_occupancy(int fg, bool hot, size_t smem_bytes, int *blocks_per_
     return hot ? occupancy_hasf_4h(smem_bytes, blocks_per_sm) : occupancy_hasf_4g(smem_bytes, blocks_per_sm);
 }
 
-int hasf_threads() { return kThreadsHost; }
+int hasf_threads() { return kHasfThreads; }
 
 }  // namespace ts

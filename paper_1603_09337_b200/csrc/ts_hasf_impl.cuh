@@ -53,7 +53,7 @@
 
 namespace ts {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = kHasfThreads;
 constexpr int kWarps = kThreads / 32;
 #ifndef TS_MIN_BLOCKS
 #define TS_MIN_BLOCKS 1
@@ -97,6 +97,11 @@ __device__ __forceinline__ Nb nbrs(const uint32_t *P, const Img &g, int p) {
     r.m = m[0];
     return r;
 }
+
+struct Row3 {   // raw words x-1, x, x+1 of one row
+    uint32_t l, c, r;
+};
+__device__ __forceinline__ Row3 row3(const uint32_t *P, int p) { return Row3{P[p - 1], P[p], P[p + 1]}; }
 
 // calls f(y, x, p) for the words of this thread's vertical strip, top to bottom
 template <class F>
@@ -303,40 +308,69 @@ __device__ __forceinline__ void cmp_step(uint32_t &lt, uint32_t &eq, uint32_t nb
 // (topo.py:225,256): ties go to the raster-earlier neighbours NW,N,NE,W.
 template <int FG, int S>
 __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
-    for_strip(g, [&](int y, int x, int p) {
-        uint32_t c = 0;
-        if (~g.B[p]) {
-            c = cand_word<FG>(g, p, t);
-            uint32_t lt[8], eq[8];
+    auto strip = [&](int x, int y0, int y1) {
+        int p = pidx(g, y0, x);
+        Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
+        Row3 ru[S], rm[S];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                lt[k] = 0;
-                eq[k] = ~0u;
-            }
-            Nb nbs[S];   // all slices' loads issued together (one L2 round trip)
-#pragma unroll
-            for (int s = 0; s < S; ++s) nbs[s] = nbrs(g.R + (size_t)s * g.plen, g, p);
-#pragma unroll
-            for (int s = S - 1; s >= 0; --s) {
-                const Nb &nb = nbs[s];
-                const uint32_t own = nb.m;
-                cmp_step(lt[0], eq[0], nb.nw, own);
-                cmp_step(lt[1], eq[1], nb.n, own);
-                cmp_step(lt[2], eq[2], nb.ne, own);
-                cmp_step(lt[3], eq[3], nb.w, own);
-                cmp_step(lt[4], eq[4], nb.e, own);
-                cmp_step(lt[5], eq[5], nb.sw, own);
-                cmp_step(lt[6], eq[6], nb.s, own);
-                cmp_step(lt[7], eq[7], nb.se, own);
-            }
-            uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
-            ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
-            ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
+        for (int s = 0; s < S; ++s) {
+            ru[s] = row3(g.R + (size_t)s * g.plen, p - g.S);
+            rm[s] = row3(g.R + (size_t)s * g.plen, p);
         }
-        g.C[p] = c;
-        g.D[p] = c;
-        append(c != 0, (uint32_t)p, g.list, counter);
-    });
+        for (int y = y0; y < y1; ++y, p += g.S) {
+            Row3 rd[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) rd[s] = row3(g.R + (size_t)s * g.plen, p + g.S);
+            const Row3 id = row3(g.I, p + g.S);
+            const uint32_t bw = g.B[p];
+            uint32_t c = 0;
+            if (~bw) {
+                const uint32_t pre = (t ? im.c : ~im.c) & ~bw;
+                if (pre)
+                    c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r),
+                                              from_west(im.l, im.c), from_east(im.c, im.r), from_west(id.l, id.c),
+                                              id.c, from_east(id.c, id.r));
+                uint32_t lt[8], eq[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    lt[k] = 0;
+                    eq[k] = ~0u;
+                }
+#pragma unroll
+                for (int s = S - 1; s >= 0; --s) {
+                    const uint32_t own = rm[s].c;
+                    cmp_step(lt[0], eq[0], from_west(ru[s].l, ru[s].c), own);
+                    cmp_step(lt[1], eq[1], ru[s].c, own);
+                    cmp_step(lt[2], eq[2], from_east(ru[s].c, ru[s].r), own);
+                    cmp_step(lt[3], eq[3], from_west(rm[s].l, rm[s].c), own);
+                    cmp_step(lt[4], eq[4], from_east(rm[s].c, rm[s].r), own);
+                    cmp_step(lt[5], eq[5], from_west(rd[s].l, rd[s].c), own);
+                    cmp_step(lt[6], eq[6], rd[s].c, own);
+                    cmp_step(lt[7], eq[7], from_east(rd[s].c, rd[s].r), own);
+                }
+                uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
+                ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
+                ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
+            }
+            g.C[p] = c;
+            g.D[p] = c;
+            append(c != 0, (uint32_t)p, g.list, counter);
+            iu = im;
+            im = id;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                ru[s] = rm[s];
+                rm[s] = rd[s];
+            }
+        }
+    };
+    const int tt = threadIdx.x;
+    if (g.WW <= kThreads) {
+        const int x = tt % g.WW, blk = tt / g.WW;
+        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb));
+    } else {
+        for (int x = tt; x < g.WW; x += kThreads) strip(x, 0, g.H);
+    }
 }
 
 // E planes straight from an int64 priority map (public homotopic_thin /
@@ -397,16 +431,16 @@ __device__ __forceinline__ uint32_t decide(uint32_t c, const Nb &i, const Nb &d,
 }
 
 // ---- dense sweeps: strip walk with a sliding 3-row window ------------------
-struct Row3 {   // raw words x-1, x, x+1 of one row
-    uint32_t l, c, r;
-};
-__device__ __forceinline__ Row3 row3(const uint32_t *P, int p) { return Row3{P[p - 1], P[p], P[p + 1]}; }
 
 // one worklist pass over the strip; returns whether any decision changed.
 // Rows are processed in groups of kDenseBatch: the group's candidate / stamp
 // checks and E loads (from L2 when E does not fit in shared memory) are issued
 // together, then the rows are evaluated in order with the sliding window.
 constexpr int kDenseBatch = 4;
+#ifndef TS_DENSE_SKIP
+#define TS_DENSE_SKIP 1
+#endif
+constexpr bool kDenseSkip = TS_DENSE_SKIP != 0;
 
 template <int FG>
 __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur, uint8_t next, int &evals) {
@@ -572,12 +606,30 @@ __device__ __forceinline__ void rebuild_sparse(const Img &g, int t, int *counter
 // recompute the candidates of every word (after a dense sweep)
 template <int FG>
 __device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter) {
-    for_strip(g, [&](int y, int x, int p) {
-        const uint32_t c = cand_word<FG>(g, p, t);
-        g.C[p] = c;
-        g.D[p] = c;
-        append(c != 0, (uint32_t)p, g.list, counter);
-    });
+    auto strip = [&](int x, int y0, int y1) {
+        int p = pidx(g, y0, x);
+        Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
+        for (int y = y0; y < y1; ++y, p += g.S) {
+            const Row3 id = row3(g.I, p + g.S);
+            const uint32_t pre = (t ? im.c : ~im.c) & ~g.B[p];
+            uint32_t c = 0;
+            if (pre)
+                c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
+                                          from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
+            g.C[p] = c;
+            g.D[p] = c;
+            append(c != 0, (uint32_t)p, g.list, counter);
+            iu = im;
+            im = id;
+        }
+    };
+    const int tt = threadIdx.x;
+    if (g.WW <= kThreads) {
+        const int x = tt % g.WW, blk = tt / g.WW;
+        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb));
+    } else {
+        for (int x = tt; x < g.WW; x += kThreads) strip(x, 0, g.H);
+    }
 }
 
 struct Stats {

@@ -12,6 +12,12 @@ namespace ts {
 // (y, x) is at (kPadRows + y) * stride + x + 1; plane length `plen` words.
 constexpr int kPadRows = 16;
 
+// threads per CTA of the fused kernel (host planning must agree)
+#ifndef TS_THREADS
+#define TS_THREADS 512
+#endif
+constexpr int kHasfThreads = TS_THREADS;
+
 enum Buf : int {
     B_I = 0,     // current image, bit-packed                          plen
     B_D,         // fixpoint decisions of the current sweep            plen
