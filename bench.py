@@ -180,6 +180,7 @@ def main():
 
     import paper_1603_09337_b200 as P
     from paper_1603_09337_b200 import _lib
+    from paper_1603_09337_b200.dist import max_over_ranks
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -223,11 +224,7 @@ def main():
         if world > 1:
             dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t_ms = float(sum(step_ms))
-    if world > 1:
-        tt = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+    t_ms = max_over_ranks(float(sum(step_ms)))
     total_images = cfg.n * world * args.steps
     value = total_images / (t_ms / 1e3)
 
@@ -262,12 +259,8 @@ def main():
         e2e_step()
     e_end.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e_start.elapsed_time(e_end)
+    e2e_ms = max_over_ranks(e_start.elapsed_time(e_end))
     wall_ms = (time.perf_counter() - t0) * 1e3
-    if world > 1:
-        tt = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
     assert np.array_equal(hout.numpy(), out.cpu().numpy())
     e2e_value = cfg.n * world * e2e_steps / (e2e_ms / 1e3)
 
