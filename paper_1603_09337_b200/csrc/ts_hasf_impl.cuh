@@ -63,6 +63,7 @@ constexpr int kMinBlocks = TS_MIN_BLOCKS;   // resident images per SM the regist
 struct Img {
     uint32_t *I, *D, *C, *B, *dirty;      // hot planes
     uint8_t *mark;                        // hot: worklist pass stamps
+    uint8_t *sflag;                       // per-strip pass stamps (null: disabled)
     uint32_t *list, *E, *XS, *R, *K, *A;  // smem or global
     int H, W, WW;
     int S;          // padded row stride (words)
@@ -408,20 +409,51 @@ __device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, in
 
 __device__ __forceinline__ bool stamped(const Img &g, int p, uint8_t cur) { return (uint8_t)(g.mark[p] - cur) <= 1; }
 
-// stamp the 3x3 word neighbourhood of p for re-evaluation in the next pass
-// (byte stores; races benign since all writers store the same value)
-__device__ __forceinline__ void stamp3x3(const Img &g, int p, uint8_t v) {
+// stamp, for re-evaluation in the next pass, the words whose inputs changed
+// when decision bits `chg` of word p flipped: column x in rows y-1..y+1, plus
+// x-1 / x+1 when an edge bit changed (byte stores; races benign since all
+// writers store the same value)
+__device__ __forceinline__ void stamp_chg(const Img &g, int p, uint32_t chg, uint8_t v) {
     uint8_t *m = g.mark + p;
     const int S = g.S;
-    m[-S - 1] = v;
     m[-S] = v;
-    m[-S + 1] = v;
-    m[-1] = v;
     m[0] = v;
-    m[1] = v;
-    m[S - 1] = v;
     m[S] = v;
-    m[S + 1] = v;
+    if (chg & 1u) {
+        m[-S - 1] = v;
+        m[-1] = v;
+        m[S - 1] = v;
+    }
+    if (chg >> 31) {
+        m[-S + 1] = v;
+        m[1] = v;
+        m[S + 1] = v;
+    }
+}
+
+// per-strip stamps (dense passes skip whole strips nothing touched).  Strip id
+// = blk * WW + x (== thread id) when WW <= kThreads, else x.
+// sid: the strip being walked (column x); top/bot: the row is the strip's
+// first / last row (its neighbour row then lies in the strip above / below)
+__device__ __forceinline__ void stamp_strips(const Img &g, int sid, int x, bool top, bool bot, uint32_t chg,
+                                             uint8_t v) {
+    if (!g.sflag) return;
+    const int up = (top && g.WW <= kThreads) ? -g.WW : 0, dn = (bot && g.WW <= kThreads) ? g.WW : 0;
+    const bool lf = (chg & 1u) && x > 0, rt = (chg >> 31) && x + 1 < g.WW;
+    uint8_t *f = g.sflag + sid;
+    f[0] = v;
+    if (up && sid + up >= 0) f[up] = v;
+    if (dn) f[dn] = v;
+    if (lf) {
+        f[-1] = v;
+        if (up && sid + up - 1 >= 0) f[up - 1] = v;
+        if (dn) f[dn - 1] = v;
+    }
+    if (rt) {
+        f[1] = v;
+        if (up && sid + up + 1 >= 0) f[up + 1] = v;
+        if (dn) f[dn + 1] = v;
+    }
 }
 
 template <int FG>
@@ -445,8 +477,9 @@ constexpr bool kDenseSkip = TS_DENSE_SKIP != 0;
 template <int FG>
 __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur, uint8_t next, int &evals) {
     bool ch = false;
-    auto strip = [&](int x, int y0, int y1) {
+    auto strip = [&](int x, int y0, int y1, int sid) {
         if (y0 >= y1) return;
+        if (!full && g.sflag && (uint8_t)(g.sflag[sid] - cur) > 1) return;   // untouched strip
         int p = pidx(g, y0, x);
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
         Row3 du = row3(g.D, p - g.S), dm = row3(g.D, p);
@@ -493,9 +526,11 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
                     const uint32_t nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
                     ++evals;
                     if (nd != dm.c) {
+                        const uint32_t chg = nd ^ dm.c;
                         g.D[p] = nd;
                         dm.c = nd;   // the next row sees this update (Gauss-Seidel down the strip)
-                        stamp3x3(g, p, next);
+                        stamp_chg(g, p, chg, next);
+                        stamp_strips(g, sid, x, yb + j == y0, yb + j == y1 - 1, chg, next);
                         ch = true;
                     }
                 }
@@ -510,9 +545,9 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
     const int t = threadIdx.x;
     if (g.WW <= kThreads) {
         const int x = t % g.WW, blk = t / g.WW;
-        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb));
+        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb), t);
     } else {
-        for (int x = t; x < g.WW; x += kThreads) strip(x, 0, g.H);
+        for (int x = t; x < g.WW; x += kThreads) strip(x, 0, g.H, x);
     }
     return ch;
 }
@@ -551,7 +586,7 @@ __device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t stamp
     dn.se = from_east(d[0], d[1]);
     const uint32_t nd = decide<FG>(s.c, s.in, dn, s.e0, s.e1);
     if (nd != s.d) {
-        if constexpr (STAMP) stamp3x3(g, s.p, stamp);
+        if constexpr (STAMP) stamp_chg(g, s.p, nd ^ s.d, stamp);
         s.d = nd;
         g.D[s.p] = nd;
         return true;
@@ -641,11 +676,17 @@ struct Stats {
     bool timing;
 };
 
+constexpr int kMaxStrips = 4096;
+#ifndef TS_STRIP_FLAGS
+#define TS_STRIP_FLAGS 0
+#endif
+
 struct Shared {
     int img;
     int counters[2];
     int bad;
     unsigned long long flips, evals;
+    uint8_t sflag[kMaxStrips];
 };
 
 // ---- phase functions ----------------------------------------------------------
@@ -694,6 +735,10 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.hb = v.hb;
     g.dense_min = v.dense_min;
     g.lastmask = v.lastmask;
+    const int nstrips = v.WW <= kThreads ? v.nblk * v.WW : v.WW;
+    g.sflag = (TS_STRIP_FLAGS && nstrips <= kMaxStrips)
+                  ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))->sflag
+                  : nullptr;
     return g;
 }
 
@@ -1005,6 +1050,8 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
     for (int q = tid; q < (g.plen + 31) >> 5; q += kThreads) g.dirty[q] = 0;
     for (int q = tid; q < (g.plen + 15) >> 4; q += kThreads)
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
+    uint8_t *sflag = shared_block(v)->sflag;
+    for (int q = tid; q < kMaxStrips; q += kThreads) sflag[q] = 0;
     __syncthreads();
     pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
     if (p.mode == MODE_THIN || p.mode == MODE_THICKEN) {
