@@ -128,6 +128,11 @@ int64_t ts_set_smem_budget(int64_t bytes);
  * (words / div) words hold candidates (default div = 8).  Returns the previous value. */
 int32_t ts_set_dense_divisor(int32_t div);
 
+/* Tuning/testing: CTAs cooperating on one image (0 = automatic: teams only for
+ * images whose hot planes exceed one SM's shared memory and when there are
+ * fewer images than co-resident CTAs).  Returns the previous value. */
+int32_t ts_set_team_size(int32_t ctas);
+
 /* Placement/occupancy the fused kernel would use for an image shape:
  * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
  * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA. */

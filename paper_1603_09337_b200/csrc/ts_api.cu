@@ -115,6 +115,7 @@ struct Plan {
     size_t smem_bytes = 0;
     uint32_t mask = 0;
     bool hot = false;
+    int team = 1;
     long long off[B_COUNT] = {};
     long long stride_ws = 0;   // global workspace words per CTA
 };
@@ -184,11 +185,14 @@ int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
     return TS_OK;
 }
 
-int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl) {
+std::atomic<int> g_team_knob{0};   // 0 = automatic team size
+
+// team = CTAs per image (> 1 only with every plane in global memory)
+int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team = 1) {
     pl.WW = (W + 31) / 32;
     if (H >= (1 << 20) || pl.WW >= (1 << 16))
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");
-    plan_strips(H, pl.WW, hasf_threads(), pl);
+    plan_strips(H, pl.WW, hasf_threads() * team, pl);
     const long long plen = (((long long)H + 2 * kPadRows) * pl.stride + 4 + 3) & ~3LL;
     if (plen * 8 >= (long long)INT_MAX)
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel (padded plane * 8 >= 2^31 words)");
@@ -214,9 +218,10 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     int sms = 0, optin = 0, per_sm = 0;
     int rc = device_props(&sms, &optin, &per_sm);
     if (rc) return rc;
-    long long budget = optin - 512;   // static shared scalars of the kernel
+    long long budget = optin - 512 - (long long)sizeof(int) * 2048;   // static Shared block of the kernel
     const long long knob = g_smem_budget.load();
     if (knob > 0 && knob < budget) budget = knob;
+    if (team > 1) budget = 0;   // teams share planes through L2
     long long used = 0, gused = 0;
     pl.mask = 0;
     for (int b = 0; b < B_COUNT; ++b) {
@@ -238,6 +243,7 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     const uint32_t hot_mask =
         (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_B) | (1u << B_DIRTY) | (1u << B_MARK);
     pl.hot = (pl.mask & hot_mask) == hot_mask;
+    pl.team = team;
     int blocks = 0;
     TS_CUDA(hasf_occupancy(fg, pl.hot, pl.smem_bytes, &blocks));
     if (blocks < 1) return fail(TS_ERR_CUDA, "fused kernel does not fit on an SM");
@@ -264,6 +270,8 @@ const char *err_message(int code, int mode) {
             return "internal: fixpoint iteration exceeded its bound";
         case ERR_SWEEP_CAP:
             return "internal: engine exceeded its sweep bound";
+        case ERR_TEAM_TIMEOUT:
+            return "internal: team barrier timed out";
         default:
             return "internal: unknown device error";
     }
@@ -296,9 +304,26 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     if (n == 0) return ok();
     Plan pl;
     if ((rc = make_plan(h, w, r_last, mode, keep != nullptr, avoid != nullptr, fg, pl))) return rc;
-    const int grid = (int)std::min<long long>(n, pl.per_wave);
-    const size_t ws_words = (size_t)pl.stride_ws * grid;
-    const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0);
+    // large images (hot planes do not fit one SM) and too few of them to fill
+    // the chip: a team of CTAs per image (rows split across the team)
+    int team = 1;
+    const int knob = g_team_knob.load();
+    if (knob > 0) {
+        team = knob;
+    } else if (!pl.hot && n < pl.per_wave) {
+        team = (int)std::min<long long>(pl.per_wave / n, std::max(1, h / 16));
+    }
+    if (team > 1) {
+        Plan pt;
+        if ((rc = make_plan(h, w, r_last, mode, keep != nullptr, avoid != nullptr, fg, pt, team))) return rc;
+        if (team > pt.per_wave) return fail(TS_ERR_UNSUPPORTED, "team larger than the co-resident CTA count");
+        pl = pt;
+    }
+    const int teams = (int)std::min<long long>(n, pl.per_wave / team);
+    const int grid = teams * team;
+    const size_t ws_words = (size_t)pl.stride_ws * (team > 1 ? teams : grid);
+    const size_t tctl_bytes = team > 1 ? (size_t)teams * kTeamCtlBytes : 0;
+    const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0) + tctl_bytes;
     char *ctrl = nullptr;
     uint32_t *gws = nullptr;
     TS_CUDA(cudaMallocAsync((void **)&ctrl, ctrl_bytes, st));
@@ -341,6 +366,8 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     p.counter = reinterpret_cast<int *>(ctrl);
     p.err = reinterpret_cast<int *>(ctrl + 16);
     p.stats = stats_host ? reinterpret_cast<long long *>(ctrl + 64) : nullptr;
+    p.team = team;
+    p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
     cudaError_t le = launch_hasf(p, fg, grid, pl.smem_bytes, st);
     int herr = 0;
     cudaError_t ce = cudaSuccess;
@@ -354,7 +381,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
     if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
     if (herr) {
-        const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP;
+        const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP || herr == ERR_TEAM_TIMEOUT;
         return fail(internal ? TS_ERR_INTERNAL : TS_ERR_VALUE, err_message(herr, mode));
     }
     return ok();
@@ -373,6 +400,8 @@ int ts_max_radius(void) { return kMaxR; }
 int64_t ts_set_smem_budget(int64_t bytes) { return g_smem_budget.exchange(bytes < 0 ? 0 : bytes); }
 
 int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 1 ? 1 : div); }
+
+int32_t ts_set_team_size(int32_t ctas) { return g_team_knob.exchange(ctas < 0 ? 0 : ctas); }
 
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {
     int rc;

@@ -72,11 +72,64 @@ struct Img {
     uint32_t lastmask;   // valid bits of the last word of a row
     int nblk, hb;        // strip mapping: row blocks per column, rows per block
     int dense_min;       // sweeps with more listed words run in dense mode
+    // team of CTAs working on this image (G == 1: this CTA alone)
+    int G, tid, nthr;    // CTAs, team thread id, team thread count
+    unsigned *bar;       // team barrier [count, generation] (G > 1)
+    unsigned *flags;     // 3 rotating "any change" flags (G > 1)
+    int *err;
+    struct Shared *sh;   // control block: shared memory (G == 1) or global (G > 1)
 };
 
 __device__ __forceinline__ int pidx(const Img &g, int y, int x) { return g.org + y * g.S + x; }
 
 __device__ __forceinline__ void set_err(int *err, int code) { atomicCAS(err, 0, code); }
+
+// Barrier over the G CTAs of a team (co-resident: cooperative launch).  Thread 0
+// of each CTA arrives on a global counter; the last one resets it and bumps the
+// generation.  The gpu-scope fences order the CTA's writes before the arrival
+// and (CCTL.IVALL) drop stale L1 lines after the release, so plane data written
+// by other CTAs is read from L2.  A spin bound turns a lost CTA into an error
+// instead of a hang.
+__device__ __forceinline__ void team_sync(const Img &g) {
+    if (g.G == 1) {
+        __syncthreads();
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = g.bar + 1;
+        const unsigned g0 = *gen;
+        __threadfence();
+        if (atomicAdd(g.bar, 1u) == (unsigned)g.G - 1) {
+            atomicExch(g.bar, 0u);
+            __threadfence();
+            atomicAdd(g.bar + 1, 1u);
+        } else {
+            long long spins = 0;
+            while (*gen == g0) {
+                __nanosleep(64);
+                if (++spins > (1LL << 26)) {   // ~ seconds
+                    set_err(g.err, ERR_TEAM_TIMEOUT);
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// team-wide OR of `v`; k = the team-uniform pass counter (rotating flags)
+__device__ __forceinline__ bool team_any(const Img &g, bool v, int k) {
+    if (g.G == 1) return __syncthreads_or(v);
+    const int any = __syncthreads_or(v);
+    if (threadIdx.x == 0) {
+        if (any) atomicOr(&g.flags[k % 3], 1u);
+        if (g.tid == 0) g.flags[(k + 1) % 3] = 0;   // next pass's flag (last read two barriers ago)
+    }
+    team_sync(g);
+    return *reinterpret_cast<volatile unsigned *>(&g.flags[k % 3]) != 0u;
+}
 
 struct Nb {
     uint32_t nw, n, ne, w, e, sw, s, se;
@@ -107,15 +160,27 @@ __device__ __forceinline__ Row3 row3(const uint32_t *P, int p) { return Row3{P[p
 // calls f(y, x, p) for the words of this thread's vertical strip, top to bottom
 template <class F>
 __device__ __forceinline__ void for_strip(const Img &g, F &&f) {
-    const int t = threadIdx.x;
-    if (g.WW <= kThreads) {
+    const int t = g.tid;
+    if (g.WW <= g.nthr) {
         const int x = t % g.WW, blk = t / g.WW;
         if (blk >= g.nblk) return;
         const int y0 = blk * g.hb, y1 = min(g.H, y0 + g.hb);
         for (int y = y0; y < y1; ++y) f(y, x, pidx(g, y, x));
     } else {
-        for (int x = t; x < g.WW; x += kThreads)
+        for (int x = t; x < g.WW; x += g.nthr)
             for (int y = 0; y < g.H; ++y) f(y, x, pidx(g, y, x));
+    }
+}
+
+// runs strip(x, y0, y1, sid) for this thread's strip(s)
+template <class F>
+__device__ __forceinline__ void walk_strips(const Img &g, F &&strip) {
+    const int t = g.tid;
+    if (g.WW <= g.nthr) {
+        const int x = t % g.WW, blk = t / g.WW;
+        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb), t);
+    } else {
+        for (int x = t; x < g.WW; x += g.nthr) strip(x, 0, g.H, x);
     }
 }
 
@@ -365,13 +430,7 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
             }
         }
     };
-    const int tt = threadIdx.x;
-    if (g.WW <= kThreads) {
-        const int x = tt % g.WW, blk = tt / g.WW;
-        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb));
-    } else {
-        for (int x = tt; x < g.WW; x += kThreads) strip(x, 0, g.H);
-    }
+    walk_strips(g, [&](int x, int y0, int y1, int) { strip(x, y0, y1); });
 }
 
 // E planes straight from an int64 priority map (public homotopic_thin /
@@ -438,7 +497,7 @@ __device__ __forceinline__ void stamp_chg(const Img &g, int p, uint32_t chg, uin
 __device__ __forceinline__ void stamp_strips(const Img &g, int sid, int x, bool top, bool bot, uint32_t chg,
                                              uint8_t v) {
     if (!g.sflag) return;
-    const int up = (top && g.WW <= kThreads) ? -g.WW : 0, dn = (bot && g.WW <= kThreads) ? g.WW : 0;
+    const int up = (top && g.WW <= g.nthr) ? -g.WW : 0, dn = (bot && g.WW <= g.nthr) ? g.WW : 0;
     const bool lf = (chg & 1u) && x > 0, rt = (chg >> 31) && x + 1 < g.WW;
     uint8_t *f = g.sflag + sid;
     f[0] = v;
@@ -542,13 +601,7 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
             }
         }
     };
-    const int t = threadIdx.x;
-    if (g.WW <= kThreads) {
-        const int x = t % g.WW, blk = t / g.WW;
-        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb), t);
-    } else {
-        for (int x = t; x < g.WW; x += kThreads) strip(x, 0, g.H, x);
-    }
+    walk_strips(g, strip);
     return ch;
 }
 
@@ -620,9 +673,9 @@ __device__ __forceinline__ unsigned apply_word(const Img &g, int p, uint32_t dw)
 // re-examine every dirty word (warp per 32-word bitmap group, lane = word)
 template <int FG>
 __device__ __forceinline__ void rebuild_sparse(const Img &g, int t, int *counter) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = g.tid >> 5;
     const int nq = (g.plen + 31) >> 5;
-    for (int q = warp; q < nq; q += kWarps) {
+    for (int q = warp; q < nq; q += g.nthr >> 5) {
         const uint32_t bits = g.dirty[q];
         if (bits == 0) continue;   // warp-uniform
         __syncwarp();
@@ -658,13 +711,7 @@ __device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter)
             im = id;
         }
     };
-    const int tt = threadIdx.x;
-    if (g.WW <= kThreads) {
-        const int x = tt % g.WW, blk = tt / g.WW;
-        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb));
-    } else {
-        for (int x = tt; x < g.WW; x += kThreads) strip(x, 0, g.H);
-    }
+    walk_strips(g, [&](int x, int y0, int y1, int) { strip(x, y0, y1); });
 }
 
 struct Stats {
@@ -689,6 +736,14 @@ struct Shared {
     uint8_t sflag[kMaxStrips];
 };
 
+// per-team control block in global memory (teams of G > 1 CTAs)
+struct TeamCtl {
+    Shared sh;
+    unsigned bar[2];
+    unsigned flags[3];
+};
+static_assert(sizeof(TeamCtl) <= kTeamCtlBytes, "kTeamCtlBytes too small");
+
 // ---- phase functions ----------------------------------------------------------
 // Each phase is a separate (non-inlined) function so that its register
 // allocation is independent of the others.  They receive the image as a View:
@@ -699,7 +754,10 @@ struct View {
     uint32_t *list, *E, *XS, *R, *K, *A;
     int H, W, WW, S, plen, org, nblk, hb, dense_min;
     uint32_t lastmask;
-    uint32_t sh;   // shared address of the CTA's Shared block
+    unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
+    int G, rank;
+    unsigned *bar, *flags;
+    int *err;
 };
 
 template <bool HOT>
@@ -735,15 +793,18 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.hb = v.hb;
     g.dense_min = v.dense_min;
     g.lastmask = v.lastmask;
-    const int nstrips = v.WW <= kThreads ? v.nblk * v.WW : v.WW;
-    g.sflag = (TS_STRIP_FLAGS && nstrips <= kMaxStrips)
-                  ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))->sflag
-                  : nullptr;
+    // HOT implies a single CTA per image: constants, so team code folds away
+    g.G = HOT ? 1 : v.G;
+    g.tid = HOT ? (int)threadIdx.x : v.rank * kThreads + (int)threadIdx.x;
+    g.nthr = HOT ? kThreads : v.G * kThreads;
+    g.bar = v.bar;
+    g.flags = v.flags;
+    g.err = v.err;
+    g.sh = g.G == 1 ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))
+                    : reinterpret_cast<Shared *>(v.sh);
+    const int nstrips = v.WW <= g.nthr ? v.nblk * v.WW : v.WW;
+    g.sflag = (TS_STRIP_FLAGS && g.G == 1 && nstrips <= kMaxStrips) ? g.sh->sflag : nullptr;
     return g;
-}
-
-__device__ __forceinline__ Shared *shared_block(const View &v) {
-    return reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh));
 }
 
 template <bool HOT, int R>
@@ -771,7 +832,7 @@ __device__ __forceinline__ int prep_dispatch_v(int r, const View &v, bool thin, 
 template <int FG, bool HOT, int S>
 __device__ __noinline__ void epass_nl(const View v, int t, int cur) {
     const Img g = make_img<HOT>(v);
-    epass_ranks<FG, S>(g, t, &shared_block(v)->counters[cur]);
+    epass_ranks<FG, S>(g, t, &g.sh->counters[cur]);
 }
 
 template <int FG, bool HOT>
@@ -791,7 +852,7 @@ static_assert(kMaxSlices <= 7, "epass_dispatch covers up to 7 rank slices");
 template <int FG, bool HOT>
 __device__ __noinline__ void epass_prio_nl(const View v, const int64_t *prio, int t, int cur) {
     const Img g = make_img<HOT>(v);
-    epass_prio<FG>(g, prio, t, &shared_block(v)->counters[cur]);
+    epass_prio<FG>(g, prio, t, &g.sh->counters[cur]);
 }
 
 struct SweepOut {
@@ -809,8 +870,9 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
     while (true) {
         const bool ch = dense_pass<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals);
         ++o.passes;
+        const bool any = team_any(g, ch, pc);
         ++pc;
-        if (!__syncthreads_or(ch)) break;
+        if (!any) break;
         if (o.passes > cap) {
             o.bad = true;
             break;
@@ -830,7 +892,7 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
 // sparse sweep over the n listed words, then apply (all threads)
 template <int FG>
 __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long cap, int pc0) {
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = g.tid, warp = tid >> 5, nthr = g.nthr;
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
     Slot s0;
@@ -861,7 +923,7 @@ __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long 
             ch = update_slot<FG, true>(g, s0, next_stamp);
             ++o.evals;
         }
-        for (int sl = tid + kThreads; sl < n; sl += kThreads) {
+        for (int sl = tid + nthr; sl < n; sl += nthr) {
             const uint32_t p = g.list[sl];
             if (!full && !stamped(g, (int)p, cur_stamp)) continue;
             Slot s;
@@ -870,15 +932,16 @@ __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long 
             ++o.evals;
         }
         ++o.passes;
+        const bool any = team_any(g, ch, pc);
         ++pc;
-        if (!__syncthreads_or(ch)) break;
+        if (!any) break;
         if (o.passes > cap) {
             o.bad = true;
             break;
         }
     }
     if (has0) o.flips += apply_word(g, s0.p, s0.d);
-    for (int sl = tid + kThreads; sl < n; sl += kThreads) {
+    for (int sl = tid + nthr; sl < n; sl += nthr) {
         const int p = (int)g.list[sl];
         o.flips += apply_word(g, p, g.D[p]);
     }
@@ -895,7 +958,7 @@ __device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int t, int
 
 // discard a prepared sweep (max_iter reached): D and C back to zero
 __device__ __forceinline__ void discard_sweep(const Img &g, int n) {
-    for (int s = threadIdx.x; s < n; s += kThreads) {
+    for (int s = g.tid; s < n; s += g.nthr) {
         const int p = (int)g.list[s];
         g.D[p] = 0;
         g.C[p] = 0;
@@ -914,23 +977,25 @@ struct EngineIO {   // engine state carried across calls (block-uniform)
 template <int FG, bool HOT>
 __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sweeps, int *err, bool timing,
                                            EngineIO io) {
+    (void)err;
     const Img g = make_img<HOT>(v);
-    Shared &sh = *shared_block(v);
-    const int tid = threadIdx.x;
+    Shared &sh = *g.sh;
+    const int tid = g.tid;
+    volatile int *vcount = sh.counters;
     int cur = io.cur, pc = io.pc;
     Stats st{};
     st.timing = timing;
     long long sweeps = 0;
     const long long sweep_cap = (long long)g.H * g.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
     while (true) {
-        const int n = sh.counters[cur];
+        const int n = vcount[cur];
         if (n == 0) break;
         if ((max_sweeps >= 0 && sweeps >= max_sweeps) || sweeps >= sweep_cap) {
             if (sweeps >= sweep_cap && (max_sweeps < 0 || sweeps < max_sweeps)) {
-                if (tid == 0) set_err(err, ERR_SWEEP_CAP);
+                if (tid == 0) set_err(g.err, ERR_SWEEP_CAP);
             }
             discard_sweep(g, n);
-            __syncthreads();
+            team_sync(g);
             break;
         }
         const long long tj0 = st.timing ? clock64() : 0;
@@ -945,12 +1010,12 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
             sh.bad = o.bad ? 1 : 0;
             sh.counters[cur ^ 1] = 0;
         }
-        __syncthreads();
-        if (sh.bad) {
-            if (tid == 0) set_err(err, ERR_JACOBI_CAP);
+        team_sync(g);
+        if (*reinterpret_cast<volatile int *>(&sh.bad)) {
+            if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
             break;
         }
-        // pass counter must stay block-uniform: tiny sweeps (one warp, no stamps)
+        // pass counter must stay team-uniform: tiny sweeps (one warp, no stamps)
         // do not advance it; dense and list sweeps count passes uniformly
         if (dense || n > 32) pc += (int)o.passes;
         if (st.timing) {
@@ -964,7 +1029,7 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
         const long long tj1 = st.timing ? clock64() : 0;
         cur ^= 1;
         rebuild_any<FG>(g, dense, t, &sh.counters[cur]);
-        __syncthreads();
+        team_sync(g);
         ++sweeps;
         st.passes += o.passes;
         if (st.timing) {
@@ -1021,38 +1086,41 @@ __device__ __forceinline__ void engine(const View &v, int t, long long max_sweep
 }
 
 template <int FG, bool HOT>
-__device__ __forceinline__ void run_stage(const View &v, int r, bool thin, int xmode, bool save_xs, Shared &sh,
-                                          int &cur, int *err, Stats &st, int &pc) {
-    if (threadIdx.x == 0) sh.counters[cur] = 0;
+__device__ __forceinline__ void run_stage(const View &v, const Img &gt, int r, bool thin, int xmode, bool save_xs,
+                                          Shared &sh, int &cur, int *err, Stats &st, int &pc) {
+    if (gt.tid == 0) sh.counters[cur] = 0;
     const long long tp0 = st.timing ? clock64() : 0;
     const int S = prep_dispatch_v<HOT>(r, v, thin, xmode, save_xs);
-    __syncthreads();
+    team_sync(gt);
     if (st.timing) st.cyc_rank += clock64() - tp0;
     epass_dispatch_v<FG, HOT>(v, S, thin ? 1 : 0, cur);
-    __syncthreads();
+    team_sync(gt);
     if (st.timing) st.cyc_prep += clock64() - tp0;
     engine<FG, HOT>(v, thin ? 1 : 0, -1, sh, cur, err, st, pc);
 }
 
-// image prologue: clear planes, pack inputs, validate (all threads)
+// image prologue: clear planes, pack inputs, validate (all team threads)
 template <bool HOT>
 __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size_t pix) {
     const KParams &p = *pp;
     const Img g = make_img<HOT>(v);
-    const int tid = threadIdx.x;
+    const int tid = g.tid, nthr = g.nthr;
     const bool has_k = p.keep != nullptr, has_a = p.avoid != nullptr;
-    for (int q = tid; q < g.plen; q += kThreads) {
+    for (int q = tid; q < g.plen; q += nthr) {
         g.I[q] = 0;
         g.D[q] = 0;
         g.C[q] = 0;
         g.B[q] = ~0u;   // pads blocked
     }
-    for (int q = tid; q < (g.plen + 31) >> 5; q += kThreads) g.dirty[q] = 0;
-    for (int q = tid; q < (g.plen + 15) >> 4; q += kThreads)
+    for (int q = tid; q < (g.plen + 31) >> 5; q += nthr) g.dirty[q] = 0;
+    for (int q = tid; q < (g.plen + 15) >> 4; q += nthr)
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
-    uint8_t *sflag = shared_block(v)->sflag;
-    for (int q = tid; q < kMaxStrips; q += kThreads) sflag[q] = 0;
-    __syncthreads();
+    if (g.G == 1) {
+        for (int q = tid; q < kMaxStrips; q += nthr) g.sh->sflag[q] = 0;
+    } else if (tid == 0) {
+        g.flags[0] = g.flags[1] = g.flags[2] = 0;
+    }
+    team_sync(g);
     pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
     if (p.mode == MODE_THIN || p.mode == MODE_THICKEN) {
         pack_plane(p.keep + pix, g.B, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
@@ -1060,7 +1128,7 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
         if (has_k) pack_plane(p.keep + pix, g.K, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
         if (has_a) pack_plane(p.avoid + pix, g.A, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
     }
-    __syncthreads();
+    team_sync(g);
     for_strip(g, [&](int y, int x, int q) {
         const uint32_t X = g.I[q];
         if (p.mode == MODE_THIN) {
@@ -1084,13 +1152,20 @@ __device__ __noinline__ void store_image_nl(const View v, uint8_t *out) {
     unpack_plane(g.I, out, g);
 }
 
+// HOT: one CTA per image, hot planes in shared memory.  !HOT: a team of
+// p.team CTAs per image (consecutive blockIdx), planes in the team's slice of
+// the global workspace, launched cooperatively when p.team > 1.
 template <int FG, bool HOT>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ Shared sh;
+    __shared__ Shared sh_local;
 
-    uint32_t *cta = p.gws + (size_t)blockIdx.x * (size_t)p.gws_stride;
+    const int G = HOT ? 1 : p.team;
+    const int team = (int)blockIdx.x / G, rank = (int)blockIdx.x - team * G;
+    uint32_t *cta = p.gws + (size_t)(G == 1 ? blockIdx.x : team) * (size_t)p.gws_stride;
     auto buf = [&](int b) -> uint32_t * { return ((p.smem_mask >> b) & 1u) ? smem + p.off[b] : cta + p.off[b]; };
+    TeamCtl *tc = G == 1 ? nullptr : reinterpret_cast<TeamCtl *>(p.tctl) + team;
+    Shared *shp = G == 1 ? &sh_local : &tc->sh;
     View v;
     if constexpr (HOT) {
         const unsigned long long base = (unsigned long long)__cvta_generic_to_shared(smem);
@@ -1124,23 +1199,30 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     v.hb = p.hb;
     v.dense_min = p.dense_min;
     v.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
-    v.sh = (uint32_t)__cvta_generic_to_shared(&sh);
+    v.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;
+    v.G = G;
+    v.rank = rank;
+    v.bar = tc ? tc->bar : nullptr;
+    v.flags = tc ? tc->flags : nullptr;
+    v.err = p.err;
+    const Img gk = make_img<HOT>(v);   // team / sync view for this function
+    Shared &sh = *shp;
     const bool has_k = p.keep != nullptr, has_a = p.avoid != nullptr;
-    const int tid = threadIdx.x;
+    const bool lead = gk.tid == 0;
 
     for (;;) {
-        if (tid == 0) sh.img = atomicAdd(p.counter, 1);
-        __syncthreads();
-        const int img = sh.img;
+        if (lead) sh.img = atomicAdd(p.counter, 1);
+        team_sync(gk);
+        const int img = *reinterpret_cast<volatile int *>(&sh.img);
         if (img >= p.n) break;
         const size_t pix = (size_t)img * p.H * p.W;
-        if (tid == 0) {
+        if (lead) {
             sh.counters[0] = 0;
             sh.flips = 0;
             sh.evals = 0;
         }
         load_image_nl<HOT>(v, &p, pix);
-        __syncthreads();
+        team_sync(gk);
 
         Stats st{};
         st.timing = p.stats != nullptr;
@@ -1155,23 +1237,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
                     const bool thin = stg == 0 || stg == 3;
                     const int xmode = (stg == 1 || stg == 3) ? 2 : ((stg == 0 ? has_k : has_a) ? 1 : 0);
                     const bool save = stg == 0 || stg == 2;
-                    run_stage<FG, HOT>(v, r, thin, xmode, save, sh, cur, p.err, st, pc);
+                    run_stage<FG, HOT>(v, gk, r, thin, xmode, save, sh, cur, p.err, st, pc);
                 }
             }
         } else {
             const int t = p.mode == MODE_THIN ? 1 : 0;
             epass_prio_nl<FG, HOT>(v, p.prio + pix, t, cur);
-            __syncthreads();
+            team_sync(gk);
             engine<FG, HOT>(v, t, p.max_sweeps, sh, cur, p.err, st, pc);
         }
 
         store_image_nl<HOT>(v, p.out + pix);
-        if (tid == 0 && p.stats) {
+        if (lead && p.stats) {
             long long *sp = p.stats + (size_t)img * kStatFields;
             sp[0] = st.sweeps;
             sp[1] = st.passes;
             sp[2] = st.calls;
-            sp[3] = (long long)sh.flips;
+            sp[3] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.flips);
             sp[4] = st.cyc_prep;
             sp[5] = st.cyc_jacobi;
             sp[6] = st.cyc_update;
@@ -1183,9 +1265,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sp[12] = st.n_dense;
             sp[13] = st.pass_dense;
             sp[14] = st.cyc_rank;
-            sp[15] = (long long)sh.evals;
+            sp[15] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.evals);
         }
-        __syncthreads();
+        team_sync(gk);
     }
 }
 
@@ -1196,6 +1278,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
         if (e != cudaSuccess) return e;                                                                         \
         void *args[] = {(void *)&p};                                                                            \
+        if (p.team > 1)                                                                                         \
+            return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);      \
         return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);                     \
     }                                                                                                           \
     cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks) {                                       \

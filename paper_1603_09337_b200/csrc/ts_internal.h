@@ -18,6 +18,9 @@ constexpr int kPadRows = 16;
 #endif
 constexpr int kHasfThreads = TS_THREADS;
 
+// bytes reserved per team control block (teams of > 1 CTA per image)
+constexpr int kTeamCtlBytes = 8192;
+
 enum Buf : int {
     B_I = 0,     // current image, bit-packed                          plen
     B_D,         // fixpoint decisions of the current sweep            plen
@@ -53,6 +56,7 @@ enum Err : int {
     ERR_KEEP_AVOID = 6,        // keep and avoid overlap
     ERR_CONSTRAINT_NOT_BINARY = 7,
     ERR_ALLOWED_NOT_SUPERSET = 8,  // thicken: object outside allowed
+    ERR_TEAM_TIMEOUT = 9,      // a team barrier did not complete (CTA not co-resident)
 };
 
 struct KParams {
@@ -65,6 +69,8 @@ struct KParams {
     int stride, plen;       // padded layout (see kPadRows)
     int nblk, hb;           // strip mapping: row blocks per word column, rows per block
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
+    int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
+    void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1)
     int r_first, r_last, do_cut, do_fill;
     int mode;
     long long max_sweeps;   // < 0: unbounded

@@ -200,3 +200,53 @@ def test_stats_are_reported():
     out, st = P.hasf_batch(imgs, 3, stats=True)
     assert st.shape == (1, 16) and st[0, 7] >= st[0, 4] + st[0, 5] > 0
     assert st[0, 2] == 12 and st[0, 0] > 0 and st[0, 1] >= st[0, 0] and st[0, 3] > 0
+
+
+@pytest.fixture
+def team_knob():
+    lib = _lib.load()
+    yield lib
+    lib.ts_set_team_size(0)
+
+
+@pytest.mark.parametrize("team", [2, 3, 5])
+def test_team_mode_vs_oracle(team_knob, team):
+    """Teams of CTAs sharing one image through L2 (the large-image path),
+    forced on small images so the oracle can check them."""
+    team_knob.ts_set_team_size(team)
+    rng = np.random.default_rng(100 + team)
+    for (h, w, fg, r) in [(160, 200, 8, 3), (97, 130, 4, 2), (64, 64, 8, 4)]:
+        imgs = np.stack([random_image(rng, h, w, rng.uniform(0.3, 0.7)) for _ in range(3)])
+        adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+        got = P.hasf_batch(imgs, r, adj)
+        assert np.array_equal(got, O.hasf_batch(imgs, r, fg, threads=4)), (team, h, w, fg)
+    img = random_image(rng, 70, 90, 0.6)
+    keep = (img & random_image(rng, 70, 90, 0.05)).astype(np.uint8)
+    pri = rng.integers(0, 7, (70, 90)).astype(np.int64)
+    for mi in (None, 2):
+        assert np.array_equal(P.homotopic_thin(img, keep, pri, P.ADJ_84, max_iter=mi),
+                              O.homotopic_thin(img, keep, pri, 8, mi))
+    allowed = (img | random_image(rng, 70, 90, 0.5)).astype(np.uint8)
+    assert np.array_equal(P.homotopic_thicken(img, allowed, pri, P.ADJ_48),
+                          O.homotopic_thicken(img, allowed, pri, 4, None))
+
+
+def test_large_image_team_auto_vs_oracle():
+    """One 2048^2 blob image (c3 generator statistics, cropped): hot planes do
+    not fit one SM, a single image -> automatic team of CTAs."""
+    img = W.blob_image(2048, 2048, 3000, objects=125, rad_lo=10, rad_hi=400, noise=0.05)
+    out = P.hasf_batch(img[None], 4)
+    assert np.array_equal(out[0], O.hasf(img, 4, 8))
+
+
+def test_c3_full_size_topology():
+    """Config c3 at full size (8192^2, r = 1..8): size-independent checks --
+    topology invariants and the sandwich of the last filling (output differs
+    from input only where smoothing acted)."""
+    cfg = W.CONFIGS["c3"]
+    img = W.config_image(cfg, 0)
+    out, st = P.hasf_batch(img[None], cfg.r_max, stats=True)
+    out = out[0]
+    assert out.shape == img.shape and out.dtype == np.uint8 and out.max() <= 1
+    assert O.topology_preserved(img, out, 8)
+    assert st[0, 2] == 4 * cfg.r_max and st[0, 3] > 0
