@@ -72,7 +72,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -172,7 +172,7 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c1", choices=sorted(W.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -316,7 +316,7 @@ def main():
                          "kernel": "ts::hasf_kernel (one launch per step)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": cfg.n * cfg.h * cfg.w,
                     "d2h_bytes_per_step": cfg.n * cfg.h * cfg.w, "wall_ms": wall_ms,
-                    "path": "ts_hasf_batch_host (C ABI, pinned host buffers)"},
+                    "path": "ts_hasf_batch_host (C ABI, pinned host buffers; chunked H2D / kernel / D2H pipeline)"},
             "gpu_launches": args.steps,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

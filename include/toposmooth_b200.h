@@ -58,8 +58,9 @@ int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
                   int32_t r_max, int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev,
                   void *stream, int64_t *stats_host);
 
-/* Same, from host buffers (copies in/out inside the call; pinned buffers are
- * copied asynchronously, pageable ones are staged by the CUDA runtime). */
+/* Same, from host buffers: the batch is pipelined in chunks (H2D copy, fused
+ * kernel and D2H copy of neighbouring chunks overlap on separate streams);
+ * page-locked buffers give asynchronous copies, pageable ones are staged. */
 int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w,
                        int32_t r_max, int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host,
                        void *stream);

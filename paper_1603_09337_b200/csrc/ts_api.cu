@@ -291,11 +291,12 @@ int check_fg(int32_t fg) {
     return TS_OK;
 }
 
-// runs the fused kernel over a batch; waits for completion and checks the
-// device error flag
-int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last,
-              int do_cut, int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, const int64_t *prio,
-              long long max_sweeps, cudaStream_t st, int64_t *stats_host) {
+// Enqueues one fused-kernel launch on `st` (workspace alloc/free stream-ordered);
+// device-side errors go to *err_dev (zeroed by the caller).  With team_out
+// non-null it receives the team size chosen.
+int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last,
+                 int do_cut, int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, const int64_t *prio,
+                 long long max_sweeps, cudaStream_t st, int64_t *stats_host, int *err_dev, int *team_out) {
     int rc;
     if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
     if (r_last > kMaxR)
@@ -324,6 +325,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     const size_t ws_words = (size_t)pl.stride_ws * (team > 1 ? teams : grid);
     const size_t tctl_bytes = team > 1 ? (size_t)teams * kTeamCtlBytes : 0;
     const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0) + tctl_bytes;
+    if (team_out) *team_out = team;
     char *ctrl = nullptr;
     uint32_t *gws = nullptr;
     TS_CUDA(cudaMallocAsync((void **)&ctrl, ctrl_bytes, st));
@@ -364,26 +366,47 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     p.hot = pl.hot ? 1 : 0;
     for (int b = 0; b < B_COUNT; ++b) p.off[b] = pl.off[b];
     p.counter = reinterpret_cast<int *>(ctrl);
-    p.err = reinterpret_cast<int *>(ctrl + 16);
+    p.err = err_dev;
     p.stats = stats_host ? reinterpret_cast<long long *>(ctrl + 64) : nullptr;
     p.team = team;
     p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
     cudaError_t le = launch_hasf(p, fg, grid, pl.smem_bytes, st);
-    int herr = 0;
     cudaError_t ce = cudaSuccess;
-    if (le == cudaSuccess) ce = cudaMemcpyAsync(&herr, ctrl + 16, sizeof(int), cudaMemcpyDeviceToHost, st);
-    if (le == cudaSuccess && ce == cudaSuccess && stats_host)
+    if (le == cudaSuccess && stats_host)
         ce = cudaMemcpyAsync(stats_host, ctrl + 64, (size_t)n * kStatFields * sizeof(long long), cudaMemcpyDeviceToHost, st);
     if (gws) cudaFreeAsync(gws, st);
     cudaFreeAsync(ctrl, st);
-    cudaError_t se = cudaStreamSynchronize(st);
     if (le != cudaSuccess) return cuda_fail(le, "launch hasf_kernel");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(stats)");
+    return TS_OK;
+}
+
+int device_error(int herr, int mode) {
+    const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP || herr == ERR_TEAM_TIMEOUT;
+    return fail(internal ? TS_ERR_INTERNAL : TS_ERR_VALUE, err_message(herr, mode));
+}
+
+// runs the fused kernel over a batch; waits for completion and checks the
+// device error flag
+int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last,
+              int do_cut, int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, const int64_t *prio,
+              long long max_sweeps, cudaStream_t st, int64_t *stats_host) {
+    if (n <= 0) return fused_launch(mode, in, out, n, h, w, r_first, r_last, do_cut, do_fill, fg, keep, avoid, prio,
+                                    max_sweeps, st, stats_host, nullptr, nullptr) ?: ok();
+    int *err = nullptr;
+    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), st));
+    cudaError_t me = cudaMemsetAsync(err, 0, sizeof(int), st);
+    int rc = me == cudaSuccess ? fused_launch(mode, in, out, n, h, w, r_first, r_last, do_cut, do_fill, fg, keep,
+                                              avoid, prio, max_sweeps, st, stats_host, err, nullptr)
+                               : cuda_fail(me, "cudaMemsetAsync");
+    int herr = 0;
+    cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(err, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (rc) return rc;
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
     if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
-    if (herr) {
-        const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP || herr == ERR_TEAM_TIMEOUT;
-        return fail(internal ? TS_ERR_INTERNAL : TS_ERR_VALUE, err_message(herr, mode));
-    }
+    if (herr) return device_error(herr, mode);
     return ok();
 }
 
@@ -426,35 +449,89 @@ int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
 
 int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w, int32_t r_max,
                        int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host, void *stream) {
+    // Pipelined: the batch is cut into chunks; chunk k's H2D copy (copy-in
+    // stream), fused kernel (compute streams, round-robin so a chunk's kernel
+    // back-fills SMs freed by the previous one) and D2H copy (copy-out stream)
+    // overlap the neighbouring chunks' work.  Page-locked buffers copy
+    // asynchronously; pageable ones are staged by the CUDA runtime.
     int rc;
-    if ((rc = check_shape(n, h, w))) return rc;
+    if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
+    if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
     if (n == 0) return ok();
-    cudaStream_t st = (cudaStream_t)stream;
-    const size_t bytes = (size_t)n * h * w;
+    cudaStream_t user = (cudaStream_t)stream;
+    const size_t img = (size_t)h * w, bytes = (size_t)n * img;
+    const bool big = (long long)h * w > 1024LL * 1024;   // team-sized images: one chunk
+    const int nchunks = big ? 1 : (int)std::min<int64_t>(n, 4);
+    const int ncs = 3;   // compute streams
+    const int64_t per = (n + nchunks - 1) / nchunks;
     uint8_t *d = nullptr;
+    int *err = nullptr;
     const int nbuf = 2 + (keep_host ? 1 : 0) + (avoid_host ? 1 : 0);
-    TS_CUDA(cudaMallocAsync((void **)&d, bytes * nbuf, st));
+    TS_CUDA(cudaMallocAsync((void **)&d, bytes * nbuf, user));
+    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
+    TS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), user));
     uint8_t *din = d, *dout = d + bytes;
     uint8_t *dk = keep_host ? d + 2 * bytes : nullptr;
     uint8_t *da = avoid_host ? d + (2 + (keep_host ? 1 : 0)) * bytes : nullptr;
-    cudaError_t e = cudaMemcpyAsync(din, in_host, bytes, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && dk) e = cudaMemcpyAsync(dk, keep_host, bytes, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && da) e = cudaMemcpyAsync(da, avoid_host, bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) {
-        cudaFreeAsync(d, st);
-        return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    cudaStream_t sin = nullptr, sout = nullptr, sc[ncs] = {};
+    std::vector<cudaEvent_t> evs;
+    auto ev = [&]() {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        evs.push_back(e);
+        return e;
+    };
+    cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
+    for (int i = 0; i < ncs && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&sc[i], cudaStreamNonBlocking);
+    cudaEvent_t ev0 = ev();
+    if (e == cudaSuccess) e = cudaEventRecord(ev0, user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, ev0, 0);
+    for (int i = 0; i < ncs && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(sc[i], ev0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev0, 0);
+    rc = TS_OK;
+    for (int k = 0; k < nchunks && e == cudaSuccess && rc == TS_OK; ++k) {
+        const int64_t i0 = k * per, cnt = std::min<int64_t>(per, n - i0);
+        if (cnt <= 0) break;
+        const size_t off = (size_t)i0 * img, sz = (size_t)cnt * img;
+        e = cudaMemcpyAsync(din + off, in_host + off, sz, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess && dk) e = cudaMemcpyAsync(dk + off, keep_host + off, sz, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess && da) e = cudaMemcpyAsync(da + off, avoid_host + off, sz, cudaMemcpyHostToDevice, sin);
+        cudaEvent_t ein = ev(), eout = ev();
+        cudaStream_t cs = sc[k % ncs];
+        if (e == cudaSuccess) e = cudaEventRecord(ein, sin);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ein, 0);
+        if (e != cudaSuccess) break;
+        rc = fused_launch(MODE_HASF, din + off, dout + off, cnt, h, w, 1, r_max, 1, 1, fg, dk ? dk + off : nullptr,
+                          da ? da + off : nullptr, nullptr, -1, cs, nullptr, err, nullptr);
+        if (rc) break;
+        e = cudaEventRecord(eout, cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, eout, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out_host + off, dout + off, sz, cudaMemcpyDeviceToHost, sout);
     }
-    rc = ts_hasf_batch(din, dout, n, h, w, r_max, fg, dk, da, stream, nullptr);
-    if (rc == TS_OK) {
-        e = cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(D2H)");
-    }
+    cudaEvent_t edone = ev();
+    cudaEventRecord(edone, sout);
+    cudaStreamWaitEvent(user, edone, 0);
+    int herr = 0;
+    cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, user);
     const std::string keep_msg = g_err;
-    cudaFreeAsync(d, st);
-    cudaStreamSynchronize(st);
-    g_err = keep_msg;
-    return rc;
+    cudaFreeAsync(d, user);
+    cudaFreeAsync(err, user);
+    cudaError_t se = cudaStreamSynchronize(user);
+    for (cudaEvent_t x : evs) cudaEventDestroy(x);
+    cudaStreamDestroy(sin);
+    cudaStreamDestroy(sout);
+    for (int i = 0; i < ncs; ++i)
+        if (sc[i]) cudaStreamDestroy(sc[i]);
+    if (rc) {
+        g_err = keep_msg;
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pipelined host path");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
+    if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
+    if (herr) return device_error(herr, MODE_HASF);
+    return ok();
 }
 
 int ts_cutting_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r, int32_t fg,

@@ -198,24 +198,47 @@ __device__ __forceinline__ uint32_t spread4(uint32_t nib) {
     return (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
 }
 
-// pack one [H,W] uint8 image into a bit-plane; flags bytes > 1
+// pack one [H,W] uint8 image into a bit-plane; flags bytes > 1.  The source
+// may be page-locked host memory read over the bus (zero-copy host entry), so
+// the loads of kPackBatch strip rows are issued before any is consumed.
+constexpr int kPackBatch = 8;
+
 __device__ __forceinline__ void pack_plane(const uint8_t *src, uint32_t *dst, const Img &g, int *err, int code) {
+    const bool fast = (g.W % 32) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    if (fast) {
+        uint32_t bad = 0;
+        walk_strips(g, [&](int x, int y0, int y1, int) {
+            for (int yb = y0; yb < y1; yb += kPackBatch) {
+                uint4 a[kPackBatch], b[kPackBatch];
+#pragma unroll
+                for (int j = 0; j < kPackBatch; ++j) {
+                    if (yb + j < y1) {
+                        const uint4 *q = reinterpret_cast<const uint4 *>(src + (size_t)(yb + j) * g.W + x * 32);
+                        a[j] = __ldg(q);
+                        b[j] = __ldg(q + 1);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kPackBatch; ++j) {
+                    if (yb + j < y1) {
+                        dst[pidx(g, yb + j, x)] = pack16(a[j]) | (pack16(b[j]) << 16);
+                        bad |= (a[j].x | a[j].y | a[j].z | a[j].w | b[j].x | b[j].y | b[j].z | b[j].w) & 0xFEFEFEFEu;
+                    }
+                }
+            }
+        });
+        if (bad) set_err(err, code);
+        return;
+    }
     for_strip(g, [&](int y, int x, int p) {
         const int c0 = x * 32;
         const int cnt = min(32, g.W - c0);
         const uint8_t *s = src + (size_t)y * g.W + c0;
         uint32_t bits = 0, bad = 0;
-        if (cnt == 32 && ((reinterpret_cast<uintptr_t>(s) & 15) == 0)) {
-            const uint4 a = __ldg(reinterpret_cast<const uint4 *>(s));
-            const uint4 b = __ldg(reinterpret_cast<const uint4 *>(s + 16));
-            bits = pack16(a) | (pack16(b) << 16);
-            bad = (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) & 0xFEFEFEFEu;
-        } else {
-            for (int i = 0; i < cnt; ++i) {
-                const uint32_t v = s[i];
-                bits |= (v & 1u) << i;
-                bad |= v & ~1u;
-            }
+        for (int i = 0; i < cnt; ++i) {
+            const uint32_t v = s[i];
+            bits |= (v & 1u) << i;
+            bad |= v & ~1u;
         }
         if (bad) set_err(err, code);
         dst[p] = bits;

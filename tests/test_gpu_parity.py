@@ -250,3 +250,15 @@ def test_c3_full_size_topology():
     assert out.shape == img.shape and out.dtype == np.uint8 and out.max() <= 1
     assert O.topology_preserved(img, out, 8)
     assert st[0, 2] == 4 * cfg.r_max and st[0, 3] > 0
+
+
+def test_host_entry_pinned_and_pageable_agree():
+    imgs = W.config_batch("c4", 40, 12)
+    want = O.hasf_batch(imgs, 4, 4, threads=4)
+    pageable = P.hasf_batch_host(imgs, 4, P.ADJ_48)                 # staged copies
+    pin_in = torch.from_numpy(imgs).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    _lib.check(_lib.load().ts_hasf_batch_host(pin_in.data_ptr(), pin_out.data_ptr(), 12, 256, 256, 4, 4, None, None,
+                                              torch.cuda.current_stream().cuda_stream))   # zero-copy
+    assert np.array_equal(pageable, want)
+    assert np.array_equal(pin_out.numpy(), want)
