@@ -126,7 +126,7 @@ int ts_selftest_circuit(uint8_t *s84_256_host, uint8_t *s48_256_host);
 int64_t ts_set_smem_budget(int64_t bytes);
 
 /* Tuning: a sweep runs in dense (strip-walk) mode when more than
- * (words / div) words hold candidates (default div = 8).  Returns the previous value. */
+ * (words / div) words hold candidates (default div = 2).  Returns the previous value. */
 int32_t ts_set_dense_divisor(int32_t div);
 
 /* Tuning/testing: CTAs cooperating on one image (0 = automatic: teams only for

@@ -120,7 +120,7 @@ struct Plan {
     long long stride_ws = 0;   // global workspace words per CTA
 };
 
-std::atomic<int> g_dense_div{8};
+std::atomic<int> g_dense_div{2};
 
 // strip mapping (thread t -> word column t % WW, row block t / WW) and the
 // padded row stride that puts the 32 lanes of every warp on distinct banks

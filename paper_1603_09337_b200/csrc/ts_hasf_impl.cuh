@@ -74,6 +74,7 @@ struct Img {
     int dense_min;       // sweeps with more listed words run in dense mode
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
+    int sx, sy0, sy1;    // this thread's strip (WW <= nthr): column, rows [sy0, sy1)
     unsigned *bar;       // team barrier [count, generation] (G > 1)
     unsigned *flags;     // 3 rotating "any change" flags (G > 1)
     int *err;
@@ -175,12 +176,10 @@ __device__ __forceinline__ void for_strip(const Img &g, F &&f) {
 // runs strip(x, y0, y1, sid) for this thread's strip(s)
 template <class F>
 __device__ __forceinline__ void walk_strips(const Img &g, F &&strip) {
-    const int t = g.tid;
     if (g.WW <= g.nthr) {
-        const int x = t % g.WW, blk = t / g.WW;
-        if (blk < g.nblk) strip(x, blk * g.hb, min(g.H, blk * g.hb + g.hb), t);
+        if (g.sy0 < g.sy1) strip(g.sx, g.sy0, g.sy1, g.tid);
     } else {
-        for (int x = t; x < g.WW; x += g.nthr) strip(x, 0, g.H, x);
+        for (int x = g.tid; x < g.WW; x += g.nthr) strip(x, 0, g.H, x);
     }
 }
 
@@ -281,6 +280,12 @@ __device__ __forceinline__ void append(bool has, uint32_t entry, uint32_t *list,
     if (lane == leader) base = atomicAdd(counter, __popc(m));
     base = __shfl_sync(act, base, leader);
     if (has) list[base + __popc(m & ((1u << lane) - 1u))] = entry;
+}
+
+// adds per-thread counts to a shared/global counter (all threads call)
+__device__ __forceinline__ void add_count(int cnt, int *counter) {
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(counter, cnt);
 }
 
 // candidates of padded word p: target-valued, unblocked, simple
@@ -397,6 +402,7 @@ __device__ __forceinline__ void cmp_step(uint32_t &lt, uint32_t &eq, uint32_t nb
 // (topo.py:225,256): ties go to the raster-earlier neighbours NW,N,NE,W.
 template <int FG, int S>
 __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
+    int cnt = 0;   // words with candidates (the list is built lazily, see build_list)
     auto strip = [&](int x, int y0, int y1) {
         int p = pidx(g, y0, x);
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
@@ -443,7 +449,7 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
             }
             g.C[p] = c;
             g.D[p] = c;
-            append(c != 0, (uint32_t)p, g.list, counter);
+            cnt += c != 0;
             iu = im;
             im = id;
 #pragma unroll
@@ -454,12 +460,14 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
         }
     };
     walk_strips(g, [&](int x, int y0, int y1, int) { strip(x, y0, y1); });
+    add_count(cnt, counter);
 }
 
 // E planes straight from an int64 priority map (public homotopic_thin /
 // homotopic_thicken: arbitrary priorities, topo.py:303-342)
 template <int FG>
 __device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, int t, int *counter) {
+    int cnt = 0;
     const int dy[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
     const int dx[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
     for_strip(g, [&](int y, int x, int p) {
@@ -485,8 +493,9 @@ __device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, in
         }
         g.C[p] = c;
         g.D[p] = c;
-        append(c != 0, (uint32_t)p, g.list, counter);
+        cnt += c != 0;
     });
+    add_count(cnt, counter);
 }
 
 __device__ __forceinline__ bool stamped(const Img &g, int p, uint8_t cur) { return (uint8_t)(g.mark[p] - cur) <= 1; }
@@ -628,6 +637,83 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
     return ch;
 }
 
+// variant for the L2-resident planes (generic / team kernel): measured faster there
+template <int FG>
+__device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, uint8_t cur, uint8_t next, int &evals) {
+    bool ch = false;
+    auto strip = [&](int x, int y0, int y1, int sid) {
+        if (y0 >= y1) return;
+        if (!full && g.sflag && (uint8_t)(g.sflag[sid] - cur) > 1) return;   // untouched strip
+        int p = pidx(g, y0, x);
+        int y = y0;
+        Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
+        Row3 du = row3(g.D, p - g.S), dm = row3(g.D, p);
+        auto step = [&](uint32_t c, uint4 e0, uint4 e1) {
+            const Row3 id = row3(g.I, p + g.S), dd = row3(g.D, p + g.S);
+            if (c) {
+                Nb in, dn;
+                in.nw = from_west(iu.l, iu.c);
+                in.n = iu.c;
+                in.ne = from_east(iu.c, iu.r);
+                in.w = from_west(im.l, im.c);
+                in.e = from_east(im.c, im.r);
+                in.sw = from_west(id.l, id.c);
+                in.s = id.c;
+                in.se = from_east(id.c, id.r);
+                dn.nw = from_west(du.l, du.c);
+                dn.n = du.c;
+                dn.ne = from_east(du.c, du.r);
+                dn.w = from_west(dm.l, dm.c);
+                dn.e = from_east(dm.c, dm.r);
+                dn.sw = from_west(dd.l, dd.c);
+                dn.s = dd.c;
+                dn.se = from_east(dd.c, dd.r);
+                const uint32_t nd = decide<FG>(c, in, dn, e0, e1);
+                ++evals;
+                if (nd != dm.c) {
+                    const uint32_t chg = nd ^ dm.c;
+                    g.D[p] = nd;
+                    dm.c = nd;
+                    stamp_chg(g, p, chg, next);
+                    stamp_strips(g, sid, x, y == y0, y == y1 - 1, chg, next);
+                    ch = true;
+                }
+            }
+            iu = im;
+            im = id;
+            du = dm;
+            dm = dd;
+            p += g.S;
+            ++y;
+        };
+        auto fetch = [&](int q, uint32_t &c, uint4 &e0, uint4 &e1) {
+            c = g.C[q];
+            if (c && !(full || stamped(g, q, cur))) c = 0;
+            if (c) {
+                const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
+                e0 = ep[0];
+                e1 = ep[1];
+            }
+        };
+        while (y + kDenseBatch <= y1) {
+            uint32_t cb[kDenseBatch];
+            uint4 e0b[kDenseBatch], e1b[kDenseBatch];
+#pragma unroll
+            for (int j = 0; j < kDenseBatch; ++j) fetch(p + j * g.S, cb[j], e0b[j], e1b[j]);
+#pragma unroll
+            for (int j = 0; j < kDenseBatch; ++j) step(cb[j], e0b[j], e1b[j]);
+        }
+        while (y < y1) {
+            uint32_t c;
+            uint4 e0, e1;
+            fetch(p, c, e0, e1);
+            step(c, e0, e1);
+        }
+    };
+    walk_strips(g, strip);
+    return ch;
+}
+
 // ---- sparse sweeps: list of words ------------------------------------------
 struct Slot {
     int p;
@@ -717,6 +803,7 @@ __device__ __forceinline__ void rebuild_sparse(const Img &g, int t, int *counter
 // recompute the candidates of every word (after a dense sweep)
 template <int FG>
 __device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter) {
+    int cnt = 0;
     auto strip = [&](int x, int y0, int y1) {
         int p = pidx(g, y0, x);
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
@@ -729,12 +816,19 @@ __device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter)
                                           from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
             g.C[p] = c;
             g.D[p] = c;
-            append(c != 0, (uint32_t)p, g.list, counter);
+            cnt += c != 0;
             iu = im;
             im = id;
         }
     };
     walk_strips(g, [&](int x, int y0, int y1, int) { strip(x, y0, y1); });
+    add_count(cnt, counter);
+}
+
+// active-word list from the C plane (needed when a sparse sweep follows a
+// dense one or the E-pass, which only count)
+__device__ __forceinline__ void build_list(const Img &g, int *counter) {
+    for_strip(g, [&](int y, int x, int p) { append(g.C[p] != 0, (uint32_t)p, g.list, counter); });
 }
 
 struct Stats {
@@ -826,6 +920,12 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.sh = g.G == 1 ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))
                     : reinterpret_cast<Shared *>(v.sh);
     const int nstrips = v.WW <= g.nthr ? v.nblk * v.WW : v.WW;
+    {
+        const int x = g.tid % v.WW, blk = g.tid / v.WW;
+        g.sx = x;
+        g.sy0 = blk < v.nblk ? blk * v.hb : 0;
+        g.sy1 = blk < v.nblk ? min(v.H, blk * v.hb + v.hb) : 0;
+    }
     g.sflag = (TS_STRIP_FLAGS && g.G == 1 && nstrips <= kMaxStrips) ? g.sh->sflag : nullptr;
     return g;
 }
@@ -886,12 +986,13 @@ struct SweepOut {
 };
 
 // dense sweep: worklist passes over the strips, then apply (all threads)
-template <int FG>
+template <int FG, bool HOT>
 __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int pc0) {
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
     while (true) {
-        const bool ch = dense_pass<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals);
+        const bool ch = HOT ? dense_pass<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals)
+                            : dense_pass_l2<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals);
         ++o.passes;
         const bool any = team_any(g, ch, pc);
         ++pc;
@@ -980,7 +1081,14 @@ __device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int t, int
 }
 
 // discard a prepared sweep (max_iter reached): D and C back to zero
-__device__ __forceinline__ void discard_sweep(const Img &g, int n) {
+__device__ __forceinline__ void discard_sweep(const Img &g, int n, bool list_ok) {
+    if (!list_ok) {
+        for_strip(g, [&](int y, int x, int p) {
+            g.D[p] = 0;
+            g.C[p] = 0;
+        });
+        return;
+    }
     for (int s = g.tid; s < n; s += g.nthr) {
         const int p = (int)g.list[s];
         g.D[p] = 0;
@@ -1010,6 +1118,7 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
     st.timing = timing;
     long long sweeps = 0;
     const long long sweep_cap = (long long)g.H * g.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
+    bool list_ok = false;   // the E-pass and dense re-examination only count candidates
     while (true) {
         const int n = vcount[cur];
         if (n == 0) break;
@@ -1017,16 +1126,23 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
             if (sweeps >= sweep_cap && (max_sweeps < 0 || sweeps < max_sweeps)) {
                 if (tid == 0) set_err(g.err, ERR_SWEEP_CAP);
             }
-            discard_sweep(g, n);
+            discard_sweep(g, n, list_ok);
             team_sync(g);
             break;
         }
         const long long tj0 = st.timing ? clock64() : 0;
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
         const bool dense = n > g.dense_min;
+        if (!dense && !list_ok) {   // sparse sweep after a counting pass: build the list
+            if (tid == 0) sh.counters[cur ^ 1] = 0;
+            team_sync(g);
+            build_list(g, &sh.counters[cur ^ 1]);
+            team_sync(g);
+            list_ok = true;
+        }
         SweepOut o;
         if (dense)
-            o = dense_sweep<FG>(g, cap, pc);
+            o = dense_sweep<FG, HOT>(g, cap, pc);
         else
             o = sparse_sweep<FG>(g, n, cap, pc);
         if (tid == 0) {
@@ -1052,6 +1168,7 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
         const long long tj1 = st.timing ? clock64() : 0;
         cur ^= 1;
         rebuild_any<FG>(g, dense, t, &sh.counters[cur]);
+        list_ok = !dense;
         team_sync(g);
         ++sweeps;
         st.passes += o.passes;

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--smem-budget", type=int, default=-1)
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--stats", type=int, default=1)
+    ap.add_argument("--dense-div", type=int, default=0)
+    ap.add_argument("--team", type=int, default=0)
     args = ap.parse_args()
     import torch
     import paper_1603_09337_b200 as P
@@ -31,11 +33,15 @@ def main():
     cfg = W.CONFIGS[args.config]
     if args.smem_budget >= 0:
         _lib.load().ts_set_smem_budget(args.smem_budget)
+    if args.dense_div > 0:
+        _lib.load().ts_set_dense_divisor(args.dense_div)
+    if args.team > 0:
+        _lib.load().ts_set_team_size(args.team)
     imgs = torch.from_numpy(W.config_batch(cfg, args.start, args.n)).cuda()
     adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
     plan = np.zeros(5, np.int64)
     _lib.load().ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
-    res = {"config": cfg.name, "n": args.n, "plan": plan.tolist()}
+    res = {"config": cfg.name, "n": args.n, "plan": plan.tolist(), "dense_div": args.dense_div, "team": args.team}
     for i in range(args.repeat):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
