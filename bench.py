@@ -292,7 +292,7 @@ def main():
             cpu = {"value": equiv / ts_, "unit": "images/s", "cores": cores, "kind": "port",
                    "sample": f"{desc}, oracle/ C restatement of the reference hasf on {cores} host "
                              f"threads, {ts_:.1f} s"}
-        plan = np.zeros(5, np.int64)
+        plan = np.zeros(6, np.int64)
         lib.ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
@@ -306,7 +306,7 @@ def main():
                        "l2": "flushed between timed steps (256 MiB fill, not timed); per-step CUDA events",
                        "plan": {"ctas_per_wave": int(plan[0]), "ctas_per_sm": int(plan[1]),
                                 "smem_bytes": int(plan[2]), "smem_mask": int(plan[3]),
-                                "gws_bytes_per_cta": int(plan[4])}},
+                                "gws_bytes_per_cta": int(plan[4]), "threads_per_cta": int(plan[5])}},
             "mpix_per_s": value * cfg.h * cfg.w / 1e6,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_from_profiles(cfg.name),

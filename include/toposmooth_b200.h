@@ -134,9 +134,14 @@ int32_t ts_set_dense_divisor(int32_t div);
  * fewer images than co-resident CTAs).  Returns the previous value. */
 int32_t ts_set_team_size(int32_t ctas);
 
+/* Tuning/testing: force the kernel flavour, 512 threads x 1 CTA/SM or 256 x 2
+ * (0 = automatic: 256 x 2 when the hot planes fit half an SM).  Returns the previous value. */
+int32_t ts_set_cta_threads(int32_t threads);
+
 /* Placement/occupancy the fused kernel would use for an image shape:
  * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
- * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA. */
+ * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA,
+ * info[5] = threads per CTA (info must hold 6 values). */
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid,
                  int64_t *info5);
 

@@ -22,8 +22,7 @@
 
 namespace ts {
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream);
-cudaError_t hasf_occupancy(int fg, bool hot, size_t smem_bytes, int *blocks_per_sm);
-int hasf_threads();
+cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm);
 cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
                               cudaStream_t st);
 cudaError_t launch_edt_phase2(const long long *g, void *out, long long *stk, int n, int H, int W, long long inf,
@@ -115,7 +114,7 @@ struct Plan {
     size_t smem_bytes = 0;
     uint32_t mask = 0;
     bool hot = false;
-    int team = 1;
+    int team = 1, threads = 512;
     long long off[B_COUNT] = {};
     long long stride_ws = 0;   // global workspace words per CTA
 };
@@ -188,11 +187,17 @@ int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
 std::atomic<int> g_team_knob{0};   // 0 = automatic team size
 
 // team = CTAs per image (> 1 only with every plane in global memory)
-int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team = 1) {
+std::atomic<int> g_threads_knob{0};   // 0 = automatic kernel flavour
+
+// one fixed flavour: `threads` per CTA, `team` CTAs per image, shared-memory
+// budget `budget_cap` bytes per CTA (<= 0: device maximum)
+int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team,
+                    int threads, long long budget_cap) {
     pl.WW = (W + 31) / 32;
     if (H >= (1 << 20) || pl.WW >= (1 << 16))
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");
-    plan_strips(H, pl.WW, hasf_threads() * team, pl);
+    pl.threads = threads;
+    plan_strips(H, pl.WW, threads * team, pl);
     const long long plen = (((long long)H + 2 * kPadRows) * pl.stride + 4 + 3) & ~3LL;
     if (plen * 8 >= (long long)INT_MAX)
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel (padded plane * 8 >= 2^31 words)");
@@ -218,7 +223,8 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     int sms = 0, optin = 0, per_sm = 0;
     int rc = device_props(&sms, &optin, &per_sm);
     if (rc) return rc;
-    long long budget = optin - 512 - (long long)sizeof(int) * 2048;   // static Shared block of the kernel
+    long long budget = optin - 512;   // static Shared block of the kernel
+    if (budget_cap > 0 && budget_cap < budget) budget = budget_cap;
     const long long knob = g_smem_budget.load();
     if (knob > 0 && knob < budget) budget = knob;
     if (team > 1) budget = 0;   // teams share planes through L2
@@ -245,11 +251,32 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     pl.hot = (pl.mask & hot_mask) == hot_mask;
     pl.team = team;
     int blocks = 0;
-    TS_CUDA(hasf_occupancy(fg, pl.hot, pl.smem_bytes, &blocks));
+    if (threads == 256 && !pl.hot) return fail(TS_ERR_UNSUPPORTED, "256-thread flavour needs the hot placement");
+    TS_CUDA(hasf_occupancy(fg, pl.hot, threads, pl.smem_bytes, &blocks));
     if (blocks < 1) return fail(TS_ERR_CUDA, "fused kernel does not fit on an SM");
     pl.per_sm = blocks;
     pl.per_wave = blocks * sms;
     return TS_OK;
+}
+
+// chooses the kernel flavour: two 256-thread CTAs per SM when the hot planes
+// fit half an SM's shared memory (small images), else one 512-thread CTA
+int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team = 1) {
+    const int knob = g_threads_knob.load();
+    if (team == 1 && knob != 512) {
+        int sms = 0, optin = 0, per_sm = 0;
+        int rc = device_props(&sms, &optin, &per_sm);
+        if (rc) return rc;
+        Plan p2;
+        const long long half = per_sm / 2 - 1024 - 512;
+        rc = make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, p2, 1, 256, half);
+        if (rc == TS_OK && p2.hot && (p2.per_sm >= 2 || knob == 256)) {
+            pl = p2;
+            return TS_OK;
+        }
+        if (knob == 256) return rc ? rc : fail(TS_ERR_UNSUPPORTED, "256-thread flavour does not fit");
+    }
+    return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, 512, 0);
 }
 
 const char *err_message(int code, int mode) {
@@ -369,6 +396,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.err = err_dev;
     p.stats = stats_host ? reinterpret_cast<long long *>(ctrl + 64) : nullptr;
     p.team = team;
+    p.threads = pl.threads;
     p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
     cudaError_t le = launch_hasf(p, fg, grid, pl.smem_bytes, st);
     cudaError_t ce = cudaSuccess;
@@ -426,6 +454,10 @@ int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 1 
 
 int32_t ts_set_team_size(int32_t ctas) { return g_team_knob.exchange(ctas < 0 ? 0 : ctas); }
 
+int32_t ts_set_cta_threads(int32_t threads) {
+    return g_threads_knob.exchange(threads == 256 || threads == 512 ? threads : 0);
+}
+
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {
     int rc;
     if ((rc = check_shape(1, h, w))) return rc;
@@ -436,6 +468,7 @@ int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t 
     info5[2] = (int64_t)pl.smem_bytes;
     info5[3] = pl.mask;
     info5[4] = pl.stride_ws * 4;
+    info5[5] = pl.threads;
     return ok();
 }
 

@@ -1,10 +1,10 @@
 // Host-side dispatch over the fused HASF kernel variants (kernel body in
-// ts_hasf_impl.cuh; one translation unit per <adjacency, placement> variant).
+// ts_hasf_impl.cuh; one translation unit per <adjacency, placement, threads>
+// variant).
 #include <cuda_runtime.h>
 #include "ts_internal.h"
 
 namespace ts {
-
 
 #define TS_DECLARE_HASF_VARIANT(SUFFIX)                                                                   \
     cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream); \
@@ -13,17 +13,26 @@ TS_DECLARE_HASF_VARIANT(8h)
 TS_DECLARE_HASF_VARIANT(8g)
 TS_DECLARE_HASF_VARIANT(4h)
 TS_DECLARE_HASF_VARIANT(4g)
+TS_DECLARE_HASF_VARIANT(8h256)
+TS_DECLARE_HASF_VARIANT(4h256)
 
+// threads: 512 (any placement) or 256 (hot placement only, two CTAs per SM)
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream) {
+    if (p.threads == 256) {
+        if (!p.hot) return cudaErrorInvalidValue;
+        return fg == 8 ? launch_hasf_8h256(p, grid, smem_bytes, stream) : launch_hasf_4h256(p, grid, smem_bytes, stream);
+    }
     if (fg == 8) return p.hot ? launch_hasf_8h(p, grid, smem_bytes, stream) : launch_hasf_8g(p, grid, smem_bytes, stream);
     return p.hot ? launch_hasf_4h(p, grid, smem_bytes, stream) : launch_hasf_4g(p, grid, smem_bytes, stream);
 }
 
-cudaError_t hasf_occupancy(int fg, bool hot, size_t smem_bytes, int *blocks_per_sm) {
+cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm) {
+    if (threads == 256) {
+        if (!hot) return cudaErrorInvalidValue;
+        return fg == 8 ? occupancy_hasf_8h256(smem_bytes, blocks_per_sm) : occupancy_hasf_4h256(smem_bytes, blocks_per_sm);
+    }
     if (fg == 8) return hot ? occupancy_hasf_8h(smem_bytes, blocks_per_sm) : occupancy_hasf_8g(smem_bytes, blocks_per_sm);
     return hot ? occupancy_hasf_4h(smem_bytes, blocks_per_sm) : occupancy_hasf_4g(smem_bytes, blocks_per_sm);
 }
-
-int hasf_threads() { return kHasfThreads; }
 
 }  // namespace ts

@@ -51,14 +51,20 @@
 #include "ts_common.cuh"
 #include "ts_internal.h"
 
-namespace ts {
-
-constexpr int kThreads = kHasfThreads;
-constexpr int kWarps = kThreads / 32;
-#ifndef TS_MIN_BLOCKS
-#define TS_MIN_BLOCKS 1
+// The body is compiled once per (threads per CTA, CTAs per SM) flavour, each in
+// its own namespace: 512 x 1 (default) and 256 x 2 (small images, two per SM).
+#ifndef TS_IMPL_THREADS
+#define TS_IMPL_THREADS 512
+#define TS_IMPL_MINB 1
+#define TS_IMPL_NS v512
 #endif
-constexpr int kMinBlocks = TS_MIN_BLOCKS;   // resident images per SM the register budget targets
+
+namespace ts {
+namespace TS_IMPL_NS {
+
+constexpr int kThreads = TS_IMPL_THREADS;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMinBlocks = TS_IMPL_MINB;   // resident images per SM the register budget targets
 
 struct Img {
     uint32_t *I, *D, *C, *B, *dirty;      // hot planes
@@ -840,10 +846,10 @@ struct Stats {
     bool timing;
 };
 
-constexpr int kMaxStrips = 4096;
 #ifndef TS_STRIP_FLAGS
 #define TS_STRIP_FLAGS 0
 #endif
+constexpr int kMaxStrips = TS_STRIP_FLAGS ? 4096 : 16;
 
 struct Shared {
     int img;
@@ -1412,8 +1418,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
 }
 
 // per-variant host entry points, one translation unit each (ts_hasf_<fg><h|g>.cu)
+}  // namespace TS_IMPL_NS
+
 #define TS_DEFINE_HASF_VARIANT(FG, HOT, SUFFIX)                                                                \
     cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream) {      \
+        using namespace TS_IMPL_NS;                                                                             \
         const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
         if (e != cudaSuccess) return e;                                                                         \
@@ -1423,6 +1432,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);                     \
     }                                                                                                           \
     cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks) {                                       \
+        using namespace TS_IMPL_NS;                                                                             \
         const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
         if (e != cudaSuccess) return e;                                                                         \

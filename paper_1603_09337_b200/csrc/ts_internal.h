@@ -70,6 +70,7 @@ struct KParams {
     int nblk, hb;           // strip mapping: row blocks per word column, rows per block
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
     int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
+    int threads;            // threads per CTA of the variant (512, or 256 = two CTAs per SM)
     void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1)
     int r_first, r_last, do_cut, do_fill;
     int mode;

@@ -262,3 +262,20 @@ def test_host_entry_pinned_and_pageable_agree():
                                               torch.cuda.current_stream().cuda_stream))   # zero-copy
     assert np.array_equal(pageable, want)
     assert np.array_equal(pin_out.numpy(), want)
+
+
+@pytest.mark.parametrize("threads", [256, 512])
+def test_kernel_flavours_vs_oracle(threads):
+    """Both compiled flavours (512 threads x 1 CTA/SM, 256 x 2) on the same inputs."""
+    lib = _lib.load()
+    old = lib.ts_set_cta_threads(threads)
+    try:
+        rng = np.random.default_rng(300 + threads)
+        for (h, w, fg, r) in [(256, 256, 4, 4), (200, 170, 8, 3), (33, 65, 8, 5)]:
+            imgs = np.stack([random_image(rng, h, w, rng.uniform(0.3, 0.7)) for _ in range(4)])
+            adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+            assert np.array_equal(P.hasf_batch(imgs, r, adj), O.hasf_batch(imgs, r, fg, threads=4)), (threads, h, w)
+        imgs = W.config_batch("c4", 700, 8)
+        assert np.array_equal(P.hasf_batch(imgs, 4, P.ADJ_48), O.hasf_batch(imgs, 4, 4, threads=4))
+    finally:
+        lib.ts_set_cta_threads(old)

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--stats", type=int, default=1)
     ap.add_argument("--dense-div", type=int, default=0)
     ap.add_argument("--team", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
     args = ap.parse_args()
     import torch
     import paper_1603_09337_b200 as P
@@ -37,9 +38,11 @@ def main():
         _lib.load().ts_set_dense_divisor(args.dense_div)
     if args.team > 0:
         _lib.load().ts_set_team_size(args.team)
+    if args.threads > 0:
+        _lib.load().ts_set_cta_threads(args.threads)
     imgs = torch.from_numpy(W.config_batch(cfg, args.start, args.n)).cuda()
     adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
-    plan = np.zeros(5, np.int64)
+    plan = np.zeros(6, np.int64)
     _lib.load().ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
     res = {"config": cfg.name, "n": args.n, "plan": plan.tolist(), "dense_div": args.dense_div, "team": args.team}
     for i in range(args.repeat):
