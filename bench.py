@@ -243,8 +243,15 @@ def main():
     total_images = cfg.n * world * args.steps
     value = total_images / (t_ms / 1e3)
 
-    # stats + correctness sample (outside the timed region)
+    # stats + correctness (outside the timed region): topology invariants of
+    # every output (device component counts), bit-exactness on a sample
     _, stats = P.hasf_batch(x, cfg.r_max, adj, stats=True)
+    fi, bi = P.topology_counts(x, adj)
+    fo, bo = P.topology_counts(out, adj)
+    topo_ok = int(np.sum((fi == fo) & (bi == bo)))
+    assert topo_ok == cfg.n, f"topology changed on {cfg.n - topo_ok} images"
+    topo_summary = {"images": cfg.n, "preserved": topo_ok,
+                    "fg_components_mean": float(fi.mean()), "bg_components_mean": float(bi.mean())}
     verified = 0
     if args.verify > 0 and rank == 0 and cfg.h * cfg.w <= 2048 * 2048:
         import oracle as O
@@ -323,6 +330,7 @@ def main():
             "engine_stats_per_image": {"sweeps": float(stats[:, 0].mean()), "fixpoint_passes": float(stats[:, 1].mean()),
                                        "engine_calls": float(stats[:, 2].mean()), "flips": float(stats[:, 3].mean())},
             "verified_images_vs_oracle": verified,
+            "topology_verified": topo_summary,
             "step_ms": step_ms,
             "paper_cpu_context_img_s": PAPER_CPU_IMG_S,
         }

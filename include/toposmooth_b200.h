@@ -113,6 +113,14 @@ int ts_neighborhood_codes_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t
 int ts_simple_point_mask_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
                                int32_t w, int32_t fg, void *stream);
 
+/* Topology verifier: number of conn-connected components (conn 4 or 8) of the
+ * object pixels (foreground = 1) or background pixels (foreground = 0) of each
+ * image; exterior = 1 attaches the window exterior to the background as one
+ * extra component (component_count / background_component_count,
+ * grid.py:93-128).  counts_host: int64[n]. */
+int ts_component_counts_batch(const uint8_t *in_dev, int64_t *counts_host, int64_t n, int32_t h, int32_t w,
+                              int32_t conn, int32_t foreground, int32_t exterior, void *stream);
+
 /* Host tables: component counts T8/T4 of every 8-bit code and the simple-point
  * LUTs (T8_TABLE, T4_TABLE, SIMPLE_84, SIMPLE_48, topo.py:79-84). */
 int ts_connectivity_tables(uint8_t *t8_256, uint8_t *t4_256, uint8_t *s84_256, uint8_t *s48_256);

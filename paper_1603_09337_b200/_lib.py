@@ -41,6 +41,7 @@ SIGNATURES = {
     "ts_neighborhood_codes_batch": ([_vp, _vp, _i64, _i32, _i32, _vp], ctypes.c_int),
     "ts_simple_point_mask_batch": ([_vp, _vp, _i64, _i32, _i32, _i32, _vp], ctypes.c_int),
     "ts_connectivity_tables": ([_vp, _vp, _vp, _vp], ctypes.c_int),
+    "ts_component_counts_batch": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int),
     "ts_selftest_circuit": ([_vp, _vp], ctypes.c_int),
     "ts_set_smem_budget": ([_i64], _i64),
     "ts_set_dense_divisor": ([_i32], _i32),

@@ -30,6 +30,8 @@ cudaError_t launch_edt_phase2(const long long *g, void *out, long long *stk, int
 cudaError_t launch_classify(const uint8_t *pix, uint8_t *out, int n, int H, int W, const uint8_t *lut,
                             cudaStream_t st);
 cudaError_t launch_selftest_circuit(uint8_t *out84, uint8_t *out48, cudaStream_t st);
+cudaError_t launch_ccl(const uint8_t *img, int *parent, long long *counts, int n, int h, int w, int conn,
+                       int target, int exterior, cudaStream_t st);
 }  // namespace ts
 
 using namespace ts;
@@ -673,6 +675,30 @@ int ts_simple_point_mask_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t 
     cudaError_t se = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "simple_point_mask");
     if (se != cudaSuccess) return cuda_fail(se, "simple_point_mask");
+    return ok();
+}
+
+int ts_component_counts_batch(const uint8_t *in_dev, int64_t *counts_host, int64_t n, int32_t h, int32_t w,
+                              int32_t conn, int32_t foreground, int32_t exterior, void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w))) return rc;
+    if (conn != 4 && conn != 8) return fail(TS_ERR_VALUE, "adjacency must be 4 or 8, got " + std::to_string(conn));
+    if ((long long)h * w + 1 >= (long long)INT_MAX) return fail(TS_ERR_UNSUPPORTED, "image too large for int32 labels");
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    int *parent = nullptr;
+    long long *cnt = nullptr;
+    TS_CUDA(cudaMallocAsync((void **)&parent, sizeof(int) * (size_t)n * ((size_t)h * w + 1), st));
+    TS_CUDA(cudaMallocAsync((void **)&cnt, sizeof(long long) * (size_t)n, st));
+    cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(long long) * (size_t)n, st);
+    if (e == cudaSuccess)
+        e = launch_ccl(in_dev, parent, cnt, (int)n, h, w, conn, foreground ? 1 : 0, exterior ? 1 : 0, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(counts_host, cnt, sizeof(long long) * (size_t)n, cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(parent, st);
+    cudaFreeAsync(cnt, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "component counts");
+    if (se != cudaSuccess) return cuda_fail(se, "component counts");
     return ok();
 }
 

@@ -279,3 +279,26 @@ def test_kernel_flavours_vs_oracle(threads):
         assert np.array_equal(P.hasf_batch(imgs, 4, P.ADJ_48), O.hasf_batch(imgs, 4, 4, threads=4))
     finally:
         lib.ts_set_cta_threads(old)
+
+
+def test_component_counts_vs_scipy():
+    rng = np.random.default_rng(77)
+    imgs = [random_image(rng, h, w, d) for (h, w, d) in [(1, 1, 1.0), (1, 1, 0.0), (5, 7, 0.5), (40, 33, 0.45),
+                                                        (64, 64, 0.6), (97, 130, 0.3), (130, 65, 0.55)]]
+    for img in imgs:
+        for n in (4, 8):
+            assert P.component_count(img, n) == O.component_count(img, n)
+            assert P.component_count(img, n, foreground=False) == O.component_count(img ^ 1, n)
+            assert P.background_component_count(img, n) == O.background_component_count(img, n)
+    batch = W.config_batch("c4", 0, 16)
+    fg, bg = P.topology_counts(batch, P.ADJ_48)
+    for k in range(16):
+        assert fg[k] == O.component_count(batch[k], 4) and bg[k] == O.background_component_count(batch[k], 8)
+
+
+def test_topology_counts_full_size_outputs():
+    img = W.config_image("c1", 9)
+    out = P.smooth(img, 5)
+    fi, bi = P.topology_counts(img[None])
+    fo, bo = P.topology_counts(out[None])
+    assert fi[0] == fo[0] == O.component_count(img, 8) and bi[0] == bo[0] == O.background_component_count(img, 4)
