@@ -9,8 +9,8 @@
 //          background "with exterior" count, window-border pixels are also
 //          united with a virtual exterior node (index h*w), which stands for the
 //          reference's one-pixel background ring (grid.py:124-128)
-//   count  roots = pixels p in the set with parent[p] == p (+ the exterior node,
-//          which always exists as a component when the exterior is attached)
+//   count  roots = pixels p in the set with parent[p] == p, plus the exterior
+//          node when it is a root itself (no border pixel in the set)
 // Hooking always points the larger root at the smaller one (atomicCAS), so the
 // forest stays acyclic; finds use path halving.
 #include <cuda_runtime.h>
@@ -100,7 +100,9 @@ __global__ void ccl_count(CclArgs a) {
         const size_t b = i / per, q = i - b * per;
         const int v = a.parent[i];
         const bool ext = q == hw;
-        if ((ext && a.exterior) || (!ext && v == (int)q)) atomicAdd((unsigned long long *)&a.counts[b], 1ull);
+        // roots only: when border pixels attached the exterior node it hangs under
+        // the smallest pixel index of that component
+        if (v == (int)q && (!ext || a.exterior)) atomicAdd((unsigned long long *)&a.counts[b], 1ull);
     }
 }
 
