@@ -190,6 +190,10 @@ std::atomic<int> g_team_knob{0};   // 0 = automatic team size
 
 // team = CTAs per image (> 1 only with every plane in global memory)
 std::atomic<int> g_threads_knob{0};   // 0 = automatic kernel flavour
+#ifndef TS_BIG_THREADS
+#define TS_BIG_THREADS 512
+#endif
+constexpr int kBigThreads = TS_BIG_THREADS;   // threads per CTA of the one-CTA-per-SM flavour
 
 // one fixed flavour: `threads` per CTA, `team` CTAs per image, shared-memory
 // budget `budget_cap` bytes per CTA (<= 0: device maximum)
@@ -265,7 +269,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
 // fit half an SM's shared memory (small images), else one 512-thread CTA
 int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team = 1) {
     const int knob = g_threads_knob.load();
-    if (team == 1 && knob != 512) {
+    if (team == 1 && knob != kBigThreads) {
         int sms = 0, optin = 0, per_sm = 0;
         int rc = device_props(&sms, &optin, &per_sm);
         if (rc) return rc;
@@ -278,7 +282,7 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         }
         if (knob == 256) return rc ? rc : fail(TS_ERR_UNSUPPORTED, "256-thread flavour does not fit");
     }
-    return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, 512, 0);
+    return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, kBigThreads, 0);
 }
 
 const char *err_message(int code, int mode) {
@@ -457,7 +461,7 @@ int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 1 
 int32_t ts_set_team_size(int32_t ctas) { return g_team_knob.exchange(ctas < 0 ? 0 : ctas); }
 
 int32_t ts_set_cta_threads(int32_t threads) {
-    return g_threads_knob.exchange(threads == 256 || threads == 512 ? threads : 0);
+    return g_threads_knob.exchange(threads == 256 || threads == kBigThreads ? threads : 0);
 }
 
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {

@@ -18,8 +18,7 @@ TS_DECLARE_HASF_VARIANT(4h256)
 
 // threads: 512 (any placement) or 256 (hot placement only, two CTAs per SM)
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream) {
-    if (p.threads == 256) {
-        if (!p.hot) return cudaErrorInvalidValue;
+    if (p.threads == 256 && p.hot) {
         return fg == 8 ? launch_hasf_8h256(p, grid, smem_bytes, stream) : launch_hasf_4h256(p, grid, smem_bytes, stream);
     }
     if (fg == 8) return p.hot ? launch_hasf_8h(p, grid, smem_bytes, stream) : launch_hasf_8g(p, grid, smem_bytes, stream);

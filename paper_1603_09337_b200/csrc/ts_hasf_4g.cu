@@ -1,4 +1,10 @@
 // Fused HASF kernel variant: foreground adjacency 4, generic (shared or global) planes.
+#ifndef TS_BIG_THREADS
+#define TS_BIG_THREADS 512
+#endif
+#define TS_IMPL_THREADS TS_BIG_THREADS
+#define TS_IMPL_MINB 1
+#define TS_IMPL_NS v512
 #include "ts_hasf_impl.cuh"
 
 namespace ts {

@@ -856,7 +856,10 @@ struct Shared {
     int counters[2];
     int bad;
     unsigned long long flips, evals;
-    uint8_t sflag[kMaxStrips];
+    union {
+        uint8_t sflag[kMaxStrips];
+        long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
+    };
 };
 
 // per-team control block in global memory (teams of G > 1 CTAs)
@@ -990,6 +993,97 @@ struct SweepOut {
     int evals;
     bool bad;
 };
+
+// Tiny-sweep regime (single-CTA images): while the list holds <= 32 words,
+// warp 0 runs whole sweeps alone -- fixpoint passes, apply, and re-examination
+// of the 3x3 word neighbourhoods of the flipped words (the words rebuild_sparse
+// would find in the dirty bitmap; the bitmap only deduplicates them here and
+// is left zero) -- with warp syncs only, no CTA barrier per sweep.  The new
+// list keeps the engine precondition; the pass counter is not advanced (tiny
+// sweeps use no stamps).  The new list length is left in counters[cur].
+struct TinyOut {
+    long long sweeps, passes, cycles;
+    unsigned flips;
+    bool bad;
+};
+
+template <int FG, bool HOT>
+__device__ __noinline__ TinyOut tiny_sweeps(const View v, int t, int cur, long long budget, bool timing) {
+    const Img g = make_img<HOT>(v);
+    const int lane = threadIdx.x & 31;
+    Shared &sh = *g.sh;
+    volatile int *vcount = sh.counters;
+    TinyOut o{0, 0, 0, 0, false};
+    const long long c0 = timing ? clock64() : 0;
+    int n = vcount[cur];
+    const unsigned lt = (1u << lane) - 1u;
+    while (n > 0 && n <= 32 && o.sweeps < budget) {
+        Slot s;
+        const bool has = lane < n;
+        if (has) load_slot<FG>(g, g.list[lane], s);
+        const long long cap = 32LL * n + 4;
+        long long np = 0;
+        while (true) {
+            const bool ch = has && update_slot<FG, false>(g, s);
+            ++np;
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, ch)) break;
+            if (np > cap) {
+                o.bad = true;
+                break;
+            }
+        }
+        o.passes += np;
+        if (o.bad) break;
+        const uint32_t dw = has ? s.d : 0u;
+        if (dw) {
+            g.I[s.p] ^= dw;
+            g.D[s.p] = 0;
+            o.flips += __popc(dw);
+        }
+        __syncwarp();
+        // 3x3 word neighbourhoods of the flipped words: first claimant (dirty
+        // bit) re-examines the word; list positions from a warp-uniform count
+        const int a = (dw & 1u) ? -1 : 0, b = (dw >> 31) ? 1 : 0;
+        const int p0 = has ? s.p : 0;
+        const bool wa = __any_sync(0xffffffffu, a != 0), wb = __any_sync(0xffffffffu, b != 0);
+        unsigned firsts = 0;   // bit k: this lane claimed word k of its neighbourhood
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            const int dy = k / 3 - 1, dx = k % 3 - 1;
+            if ((dx < 0 && !wa) || (dx > 0 && !wb)) continue;   // warp-uniform
+            const int q = p0 + dy * g.S + dx;
+            bool first = false;
+            if (dw && dx >= a && dx <= b) {
+                const uint32_t bit = 1u << (q & 31);
+                first = !(atomicOr(&g.dirty[q >> 5], bit) & bit);
+            }
+            uint32_t c = 0;
+            if (first) {
+                firsts |= 1u << k;
+                c = cand_word<FG>(g, q, t);
+                g.C[q] = c;
+                g.D[q] = c;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, c != 0);
+            if (c) g.list[cnt + __popc(m & lt)] = (uint32_t)q;
+            cnt += __popc(m);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+            if ((firsts >> k) & 1u) g.dirty[(p0 + (k / 3 - 1) * g.S + k % 3 - 1) >> 5] = 0;
+        __syncwarp();
+        n = cnt;
+        ++o.sweeps;
+    }
+    if (lane == 0) sh.counters[cur] = n;
+    __syncwarp();
+    o.flips = __reduce_add_sync(0xffffffffu, o.flips);
+    if (timing) o.cycles = clock64() - c0;
+    return o;
+}
 
 // dense sweep: worklist passes over the strips, then apply (all threads)
 template <int FG, bool HOT>
@@ -1138,13 +1232,43 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
         }
         const long long tj0 = st.timing ? clock64() : 0;
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
-        const bool dense = n > g.dense_min;
+        const bool tiny = g.G == 1 && n <= 32;   // warp-resident regime (needs the list)
+        const bool dense = n > g.dense_min && !tiny;
         if (!dense && !list_ok) {   // sparse sweep after a counting pass: build the list
             if (tid == 0) sh.counters[cur ^ 1] = 0;
             team_sync(g);
             build_list(g, &sh.counters[cur ^ 1]);
             team_sync(g);
             list_ok = true;
+        }
+        if (tiny) {
+            long long budget = sweep_cap - sweeps;
+            if (max_sweeps >= 0) budget = min(budget, max_sweeps - sweeps);
+            if (tid < 32) {
+                const TinyOut to = tiny_sweeps<FG, HOT>(v, t, cur, budget, st.timing);
+                if (tid == 0) {
+                    sh.bad = to.bad ? 1 : 0;
+                    sh.tiny[0] = to.sweeps;
+                    sh.tiny[1] = to.passes;
+                    if (st.timing) {
+                        st.cyc_tiny += to.cycles;
+                        st.cyc_jacobi += to.cycles;
+                        st.n_tiny += to.sweeps;
+                        st.pass_tiny += to.passes;
+                        atomicAdd(&sh.flips, (unsigned long long)to.flips);
+                    }
+                }
+            }
+            __syncthreads();
+            sweeps += *reinterpret_cast<volatile long long *>(&sh.tiny[0]);
+            st.passes += *reinterpret_cast<volatile long long *>(&sh.tiny[1]);
+            const bool tbad = *reinterpret_cast<volatile int *>(&sh.bad) != 0;
+            __syncthreads();   // shared results read before they can be rewritten
+            if (tbad) {
+                if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
+                break;
+            }
+            continue;
         }
         SweepOut o;
         if (dense)
