@@ -1003,6 +1003,7 @@ struct SweepOut {
 // sweeps use no stamps).  The new list length is left in counters[cur].
 struct TinyOut {
     long long sweeps, passes, cycles;
+    long long ph[3];   // TS_TINY_PROF: load+passes, apply+claim, re-examination cycles
     unsigned flips;
     bool bad;
 };
@@ -1012,12 +1013,14 @@ __device__ __noinline__ TinyOut tiny_sweeps(const View v, int t, int cur, long l
     const Img g = make_img<HOT>(v);
     const int lane = threadIdx.x & 31;
     Shared &sh = *g.sh;
-    volatile int *vcount = sh.counters;
-    TinyOut o{0, 0, 0, 0, false};
+    TinyOut o{0, 0, 0, {0, 0, 0}, 0, false};
     const long long c0 = timing ? clock64() : 0;
-    int n = vcount[cur];
+    int n = *reinterpret_cast<volatile int *>(&sh.counters[cur]);
     const unsigned lt = (1u << lane) - 1u;
     while (n > 0 && n <= 32 && o.sweeps < budget) {
+#ifdef TS_TINY_PROF
+        long long tq = clock64();
+#endif
         Slot s;
         const bool has = lane < n;
         if (has) load_slot<FG>(g, g.list[lane], s);
@@ -1035,6 +1038,9 @@ __device__ __noinline__ TinyOut tiny_sweeps(const View v, int t, int cur, long l
         }
         o.passes += np;
         if (o.bad) break;
+#ifdef TS_TINY_PROF
+        { const long long t1 = clock64(); o.ph[0] += t1 - tq; tq = t1; }
+#endif
         const uint32_t dw = has ? s.d : 0u;
         if (dw) {
             g.I[s.p] ^= dw;
@@ -1042,41 +1048,66 @@ __device__ __noinline__ TinyOut tiny_sweeps(const View v, int t, int cur, long l
             o.flips += __popc(dw);
         }
         __syncwarp();
-        // 3x3 word neighbourhoods of the flipped words: first claimant (dirty
-        // bit) re-examines the word; list positions from a warp-uniform count
+        // 3x3 word neighbourhoods of the flipped words: the first claimant
+        // (dirty bit; all claims in flight together) queues the word at the
+        // list head, then the queue is re-examined 32 words at a time and
+        // compacted in place into the new list (writes trail the reads)
         const int a = (dw & 1u) ? -1 : 0, b = (dw >> 31) ? 1 : 0;
         const int p0 = has ? s.p : 0;
-        const bool wa = __any_sync(0xffffffffu, a != 0), wb = __any_sync(0xffffffffu, b != 0);
-        unsigned firsts = 0;   // bit k: this lane claimed word k of its neighbourhood
-        int cnt = 0;
+        unsigned firsts = 0;
+        if (dw) {
+            uint32_t bit[9], old[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {   // branch-free: the 9 atomics issue back to back
+                const int dx = k % 3 - 1;
+                const int q = p0 + (k / 3 - 1) * g.S + dx;
+                bit[k] = (dx >= a && dx <= b) ? 1u << (q & 31) : 0u;
+                old[k] = atomicOr(&g.dirty[q >> 5], bit[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                if (bit[k] & ~old[k]) firsts |= 1u << k;
+        }
+        const unsigned any_first = __reduce_or_sync(0xffffffffu, firsts);
+        int m = 0;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            const int dy = k / 3 - 1, dx = k % 3 - 1;
-            if ((dx < 0 && !wa) || (dx > 0 && !wb)) continue;   // warp-uniform
-            const int q = p0 + dy * g.S + dx;
-            bool first = false;
-            if (dw && dx >= a && dx <= b) {
-                const uint32_t bit = 1u << (q & 31);
-                first = !(atomicOr(&g.dirty[q >> 5], bit) & bit);
-            }
+            if (!((any_first >> k) & 1u)) continue;   // warp-uniform
+            const bool first = (firsts >> k) & 1u;
+            const unsigned fm = __ballot_sync(0xffffffffu, first);
+            if (first) g.list[m + __popc(fm & lt)] = (uint32_t)(p0 + (k / 3 - 1) * g.S + k % 3 - 1);
+            m += __popc(fm);
+        }
+        __syncwarp();
+#ifdef TS_TINY_PROF
+        { const long long t1 = clock64(); o.ph[1] += t1 - tq; tq = t1; }
+#endif
+        int cnt = 0;
+        for (int base = 0; base < m; base += 32) {
+            const bool in = base + lane < m;
+            const int q = in ? (int)g.list[base + lane] : 0;
+            __syncwarp();
             uint32_t c = 0;
-            if (first) {
-                firsts |= 1u << k;
+            if (in) {
+                g.dirty[q >> 5] = 0;
                 c = cand_word<FG>(g, q, t);
                 g.C[q] = c;
                 g.D[q] = c;
             }
-            const unsigned m = __ballot_sync(0xffffffffu, c != 0);
-            if (c) g.list[cnt + __popc(m & lt)] = (uint32_t)q;
-            cnt += __popc(m);
+            const unsigned cm = __ballot_sync(0xffffffffu, c != 0);
+            if (c) {
+                g.list[cnt + __popc(cm & lt)] = (uint32_t)q;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(g.E + (size_t)q * 8));
+            }
+            cnt += __popc(cm);
+            __syncwarp();
         }
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < 9; ++k)
-            if ((firsts >> k) & 1u) g.dirty[(p0 + (k / 3 - 1) * g.S + k % 3 - 1) >> 5] = 0;
-        __syncwarp();
         n = cnt;
+        __syncwarp();
         ++o.sweeps;
+#ifdef TS_TINY_PROF
+        o.ph[2] += clock64() - tq;
+#endif
     }
     if (lane == 0) sh.counters[cur] = n;
     __syncwarp();
@@ -1199,6 +1230,9 @@ __device__ __forceinline__ void discard_sweep(const Img &g, int n, bool list_ok)
 // the priority-ordered flip engine (topo.py:211-258), see file header.
 // Precondition (after a __syncthreads): C = candidates of every word, D = C,
 // list = words with C != 0, counters[cur] = its size, dirty bitmap zero.
+#ifndef TS_ENGINE_INLINE
+#define TS_ENGINE_INLINE __noinline__
+#endif
 struct EngineIO {   // engine state carried across calls (block-uniform)
     int cur, pc;
     long long sweeps, passes, calls;
@@ -1206,7 +1240,7 @@ struct EngineIO {   // engine state carried across calls (block-uniform)
 };
 
 template <int FG, bool HOT>
-__device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sweeps, int *err, bool timing,
+__device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long max_sweeps, int *err, bool timing,
                                            EngineIO io) {
     (void)err;
     const Img g = make_img<HOT>(v);
@@ -1255,6 +1289,11 @@ __device__ __noinline__ EngineIO engine_nl(const View v, int t, long long max_sw
                         st.cyc_jacobi += to.cycles;
                         st.n_tiny += to.sweeps;
                         st.pass_tiny += to.passes;
+#ifdef TS_TINY_PROF
+                        st.cyc_dense += to.ph[0];
+                        st.pass_dense += to.ph[1];
+                        st.cyc_update += to.ph[2];
+#endif
                         atomicAdd(&sh.flips, (unsigned long long)to.flips);
                     }
                 }
@@ -1339,7 +1378,13 @@ __device__ __forceinline__ void engine(const View &v, int t, long long max_sweep
     EngineIO io{};
     io.cur = cur;
     io.pc = pc;
+#ifdef TS_PROF2
+    const long long te0 = clock64();
+#endif
     io = engine_nl<FG, HOT>(v, t, max_sweeps, err, st.timing, io);
+#ifdef TS_PROF2
+    st.cyc_rank += clock64() - te0;   // profiling build: whole engine calls
+#endif
     cur = io.cur;
     pc = io.pc;
     st.sweeps += io.sweeps;
