@@ -566,6 +566,9 @@ __device__ __forceinline__ uint32_t decide(uint32_t c, const Nb &i, const Nb &d,
 // checks and E loads (from L2 when E does not fit in shared memory) are issued
 // together, then the rows are evaluated in order with the sliding window.
 constexpr int kDenseBatch = 4;
+#ifndef TS_WORD_FIX
+#define TS_WORD_FIX 1
+#endif
 #ifndef TS_DENSE_SKIP
 #define TS_DENSE_SKIP 1
 #endif
@@ -620,7 +623,17 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
                     dn.sw = from_west(dd.l, dd.c);
                     dn.s = dd.c;
                     dn.se = from_east(dd.c, dd.r);
-                    const uint32_t nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
+                    uint32_t nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
+#if TS_WORD_FIX
+                    // resolve chains inside the word now: re-decide with the
+                    // word's own new decisions as its W/E neighbours
+                    for (uint32_t pd = dm.c; nd != pd;) {
+                        pd = nd;
+                        dn.w = from_west(dm.l, nd);
+                        dn.e = from_east(nd, dm.r);
+                        nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
+                    }
+#endif
                     ++evals;
                     if (nd != dm.c) {
                         const uint32_t chg = nd ^ dm.c;
