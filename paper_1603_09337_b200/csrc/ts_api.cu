@@ -111,7 +111,8 @@ const Tables &tables() {
 // ---- fused-kernel planning ------------------------------------------------
 struct Plan {
     int WW = 0, nwords = 0, slices = 0;
-    int stride = 0, plen = 0, nblk = 1, hb = 1, dense_min = 0;
+    int stride = 0, plen = 0, nblk = 1, hb = 1, nstrips = 1, dense_min = 0;
+    int pad = kPadRows;
     int per_sm = 0, per_wave = 0;
     size_t smem_bytes = 0;
     uint32_t mask = 0;
@@ -125,12 +126,14 @@ std::atomic<int> g_dense_div{2};
 
 // strip mapping (thread t -> word column t % WW, row block t / WW) and the
 // padded row stride that puts the 32 lanes of every warp on distinct banks
-void plan_strips(int H, int WW, int threads, Plan &pl) {
+// returns the worst bank multiplicity of a warp's first-row accesses
+int plan_strips(int H, int WW, int threads, Plan &pl) {
     if (WW > threads) {
         pl.nblk = 1;
         pl.hb = H;
         pl.stride = WW + 1;
-        return;
+        pl.nstrips = WW;
+        return 1;
     }
     int nblk = std::min(threads / WW, H);
     const int hb = (H + nblk - 1) / nblk;
@@ -157,6 +160,8 @@ void plan_strips(int H, int WW, int threads, Plan &pl) {
         if (best_cost == 1) break;
     }
     pl.stride = best_s;
+    pl.nstrips = nblk * WW;
+    return best_cost;
 }
 
 // Keep freed workspace in the device's stream-ordered pool across calls (the
@@ -203,8 +208,14 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     if (H >= (1 << 20) || pl.WW >= (1 << 16))
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");
     pl.threads = threads;
-    plan_strips(H, pl.WW, threads * team, pl);
-    const long long plen = (((long long)H + 2 * kPadRows) * pl.stride + 4 + 3) & ~3LL;
+    // strips: one per thread, or two when that leaves a warp's strips on
+    // conflicting banks (e.g. 256 threads on 16-word rows: 32-row blocks)
+    if (plan_strips(H, pl.WW, threads * team, pl) > 1 && team == 1) {
+        Plan p2 = pl;
+        if (plan_strips(H, pl.WW, 2 * threads, p2) == 1) pl = p2;
+    }
+    pl.pad = kPadRows;
+    const long long plen = (((long long)H + 2 * pl.pad) * pl.stride + 4 + 3) & ~3LL;
     if (plen * 8 >= (long long)INT_MAX)
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel (padded plane * 8 >= 2^31 words)");
     pl.plen = (int)plen;
@@ -236,7 +247,8 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     if (team > 1) budget = 0;   // teams share planes through L2
     long long used = 0, gused = 0;
     pl.mask = 0;
-    for (int b = 0; b < B_COUNT; ++b) {
+    for (int i = 0; i < B_COUNT; ++i) {
+        const int b = kPlaceOrder[i];
         if (size[b] == 0) {
             pl.off[b] = 0;
             continue;
@@ -253,7 +265,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     pl.smem_bytes = (size_t)(used * 4);
     pl.stride_ws = gused;
     const uint32_t hot_mask =
-        (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_B) | (1u << B_DIRTY) | (1u << B_MARK);
+        (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_DIRTY) | (1u << B_MARK);
     pl.hot = (pl.mask & hot_mask) == hot_mask;
     pl.team = team;
     int blocks = 0;
@@ -276,7 +288,9 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         Plan p2;
         const long long half = per_sm / 2 - 1024 - 512;
         rc = make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, p2, 1, 256, half);
-        if (rc == TS_OK && p2.hot && (p2.per_sm >= 2 || knob == 256)) {
+        // (measured: two images per SM pay off only when each thread walks a
+        // single strip; with two strips per thread c1 ran 10% slower)
+        if (rc == TS_OK && p2.hot && ((p2.per_sm >= 2 && p2.nstrips <= 256) || knob == 256)) {
             pl = p2;
             return TS_OK;
         }
@@ -394,6 +408,8 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.plen = pl.plen;
     p.nblk = pl.nblk;
     p.hb = pl.hb;
+    p.nstrips = pl.nstrips;
+    p.pad = pl.pad;
     p.dense_min = pl.dense_min;
     p.smem_mask = pl.mask;
     p.hot = pl.hot ? 1 : 0;

@@ -39,7 +39,7 @@
 // After the first pass of a sweep only words stamped by a changed neighbour
 // decision are re-evaluated (a worklist of per-word pass stamps).
 //
-// Layout: every plane is padded with kPadRows zero rows above and below and
+// Layout: every plane is padded with one zero row above and below and
 // one zero word between rows (row stride S >= WW + 1, chosen on the host so
 // the 32 lanes of a warp touch 32 distinct banks), so neighbour and disc
 // accesses need no bounds checks.  The hot planes (I, D, C, B, the dirty
@@ -67,20 +67,19 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMinBlocks = TS_IMPL_MINB;   // resident images per SM the register budget targets
 
 struct Img {
-    uint32_t *I, *D, *C, *B, *dirty;      // hot planes
-    uint8_t *mark;                        // hot: worklist pass stamps
-    uint8_t *sflag;                       // per-strip pass stamps (null: disabled)
-    uint32_t *list, *E, *XS, *R, *K, *A;  // smem or global
+    uint32_t *I, *D, *C, *dirty;          // hot planes
+    uint8_t *mark;                        // hot: worklist pass stamps, one byte per word
+    uint32_t *B, *list, *E, *XS, *R, *K, *A;  // smem or global (generic pointers)
     int H, W, WW;
     int S;          // padded row stride (words)
     int plen;       // padded plane length (words)
     int org;        // index of word (0, 0)
     uint32_t lastmask;   // valid bits of the last word of a row
     int nblk, hb;        // strip mapping: row blocks per column, rows per block
+    int nstrips;         // nblk * WW strips; thread walks strips tid, tid + nthr, ...
     int dense_min;       // sweeps with more listed words run in dense mode
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
-    int sx, sy0, sy1;    // this thread's strip (WW <= nthr): column, rows [sy0, sy1)
     unsigned *bar;       // team barrier [count, generation] (G > 1)
     unsigned *flags;     // 3 rotating "any change" flags (G > 1)
     int *err;
@@ -164,29 +163,26 @@ struct Row3 {   // raw words x-1, x, x+1 of one row
 };
 __device__ __forceinline__ Row3 row3(const uint32_t *P, int p) { return Row3{P[p - 1], P[p], P[p + 1]}; }
 
-// calls f(y, x, p) for the words of this thread's vertical strip, top to bottom
+// runs strip(x, y0, y1, sid) for this thread's strips: strip s = blk * WW + x
+// covers column x, rows [blk * hb, blk * hb + hb); thread t walks s = t,
+// t + nthr, ...  (the host picks nblk / hb / stride so that the strips a warp
+// walks together hit distinct shared-memory banks)
 template <class F>
-__device__ __forceinline__ void for_strip(const Img &g, F &&f) {
-    const int t = g.tid;
-    if (g.WW <= g.nthr) {
-        const int x = t % g.WW, blk = t / g.WW;
-        if (blk >= g.nblk) return;
-        const int y0 = blk * g.hb, y1 = min(g.H, y0 + g.hb);
-        for (int y = y0; y < y1; ++y) f(y, x, pidx(g, y, x));
-    } else {
-        for (int x = t; x < g.WW; x += g.nthr)
-            for (int y = 0; y < g.H; ++y) f(y, x, pidx(g, y, x));
+__device__ __forceinline__ void walk_strips(const Img &g, F &&strip) {
+    // one call site: the strip body is inlined once
+    for (int s = g.tid; s < g.nstrips; s += g.nthr) {
+        const int blk = s / g.WW, x = s - blk * g.WW;
+        const int y0 = blk * g.hb;
+        strip(x, y0, min(g.H, y0 + g.hb), s);
     }
 }
 
-// runs strip(x, y0, y1, sid) for this thread's strip(s)
+// calls f(y, x, p) for the words of this thread's strips, top to bottom
 template <class F>
-__device__ __forceinline__ void walk_strips(const Img &g, F &&strip) {
-    if (g.WW <= g.nthr) {
-        if (g.sy0 < g.sy1) strip(g.sx, g.sy0, g.sy1, g.tid);
-    } else {
-        for (int x = g.tid; x < g.WW; x += g.nthr) strip(x, 0, g.H, x);
-    }
+__device__ __forceinline__ void for_strip(const Img &g, F &&f) {
+    walk_strips(g, [&](int x, int y0, int y1, int) {
+        for (int y = y0; y < y1; ++y) f(y, x, pidx(g, y, x));
+    });
 }
 
 // ---- bit packing of uint8 {0,1} images ---------------------------------
@@ -337,18 +333,20 @@ __device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, boo
     using LV = Lev<R>;
     constexpr int L = LV::L;
     constexpr int S = LV::S;
-    static_assert(R <= kPadRows, "disc rows must stay inside the padded frame");
     const uint32_t inv = thin ? ~0u : 0u;
     const int SS = g.S;
     for_strip(g, [&](int y, int x, int p) {
         const uint32_t *c = g.I + p;
+        // rows beyond the frame read the single zero pad row (-1 or H): all
+        // exterior rows are equal, so the disc needs no deeper padding
+        const int up = y + 1, dn = g.H - y;
         uint32_t V[R + 1][3];
         V[0][0] = c[-1] ^ inv;
         V[0][1] = c[0] ^ inv;
         V[0][2] = c[1] ^ inv;
 #pragma unroll
         for (int k = 1; k <= R; ++k) {
-            const uint32_t *a = c - k * SS, *b = c + k * SS;
+            const uint32_t *a = c - min(k, up) * SS, *b = c + min(k, dn) * SS;
             V[k][0] = V[k - 1][0] | (a[-1] ^ inv) | (b[-1] ^ inv);
             V[k][1] = V[k - 1][1] | (a[0] ^ inv) | (b[0] ^ inv);
             V[k][2] = V[k - 1][2] | (a[1] ^ inv) | (b[1] ^ inv);
@@ -504,12 +502,23 @@ __device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, in
     add_count(cnt, counter);
 }
 
-__device__ __forceinline__ bool stamped(const Img &g, int p, uint8_t cur) { return (uint8_t)(g.mark[p] - cur) <= 1; }
+// ---- fixpoint worklist: per-word pass stamps --------------------------------
+// Pass k (k = the team-uniform pass counter) re-evaluates the words stamped
+// k (by pass k - 1) or k + 1 (earlier in pass k) and stamps k + 1; stamps are
+// the counter's low byte (byte stores: all writers of a word store the same
+// value, so no atomics).  A stale stamp only costs an extra evaluation (any
+// evaluation order reaches the same fixpoint).
+struct Marks {
+    uint8_t cur, next;
+};
+
+__device__ __forceinline__ Marks pass_marks(const Img &, int k) { return Marks{(uint8_t)k, (uint8_t)(k + 1)}; }
+
+__device__ __forceinline__ bool stamped(const Img &g, const Marks &m, int p) { return (uint8_t)(g.mark[p] - m.cur) <= 1; }
 
 // stamp, for re-evaluation in the next pass, the words whose inputs changed
 // when decision bits `chg` of word p flipped: column x in rows y-1..y+1, plus
-// x-1 / x+1 when an edge bit changed (byte stores; races benign since all
-// writers store the same value)
+// x-1 / x+1 when an edge bit changed
 __device__ __forceinline__ void stamp_chg(const Img &g, int p, uint32_t chg, uint8_t v) {
     uint8_t *m = g.mark + p;
     const int S = g.S;
@@ -525,31 +534,6 @@ __device__ __forceinline__ void stamp_chg(const Img &g, int p, uint32_t chg, uin
         m[-S + 1] = v;
         m[1] = v;
         m[S + 1] = v;
-    }
-}
-
-// per-strip stamps (dense passes skip whole strips nothing touched).  Strip id
-// = blk * WW + x (== thread id) when WW <= kThreads, else x.
-// sid: the strip being walked (column x); top/bot: the row is the strip's
-// first / last row (its neighbour row then lies in the strip above / below)
-__device__ __forceinline__ void stamp_strips(const Img &g, int sid, int x, bool top, bool bot, uint32_t chg,
-                                             uint8_t v) {
-    if (!g.sflag) return;
-    const int up = (top && g.WW <= g.nthr) ? -g.WW : 0, dn = (bot && g.WW <= g.nthr) ? g.WW : 0;
-    const bool lf = (chg & 1u) && x > 0, rt = (chg >> 31) && x + 1 < g.WW;
-    uint8_t *f = g.sflag + sid;
-    f[0] = v;
-    if (up && sid + up >= 0) f[up] = v;
-    if (dn) f[dn] = v;
-    if (lf) {
-        f[-1] = v;
-        if (up && sid + up - 1 >= 0) f[up - 1] = v;
-        if (dn) f[dn - 1] = v;
-    }
-    if (rt) {
-        f[1] = v;
-        if (up && sid + up + 1 >= 0) f[up + 1] = v;
-        if (dn) f[dn + 1] = v;
     }
 }
 
@@ -575,11 +559,11 @@ constexpr int kDenseBatch = 4;
 constexpr bool kDenseSkip = TS_DENSE_SKIP != 0;
 
 template <int FG>
-__device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur, uint8_t next, int &evals) {
+__device__ __forceinline__ bool dense_pass(const Img &g, bool full, int pc, int &evals) {
     bool ch = false;
-    auto strip = [&](int x, int y0, int y1, int sid) {
+    const Marks mk = pass_marks(g, pc);
+    auto strip = [&](int x, int y0, int y1, int) {
         if (y0 >= y1) return;
-        if (!full && g.sflag && (uint8_t)(g.sflag[sid] - cur) > 1) return;   // untouched strip
         int p = pidx(g, y0, x);
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
         Row3 du = row3(g.D, p - g.S), dm = row3(g.D, p);
@@ -592,7 +576,7 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
                 cb[j] = 0;
                 if (yb + j < y1) {
                     const uint32_t c = g.C[q];
-                    if (c && (full || stamped(g, q, cur))) {
+                    if (c && (full || stamped(g, mk, q))) {
                         cb[j] = c;
                         const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
                         e0b[j] = ep[0];
@@ -639,8 +623,7 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
                         const uint32_t chg = nd ^ dm.c;
                         g.D[p] = nd;
                         dm.c = nd;   // the next row sees this update (Gauss-Seidel down the strip)
-                        stamp_chg(g, p, chg, next);
-                        stamp_strips(g, sid, x, yb + j == y0, yb + j == y1 - 1, chg, next);
+                        stamp_chg(g, p, chg, mk.next);
                         ch = true;
                     }
                 }
@@ -658,11 +641,11 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, uint8_t cur,
 
 // variant for the L2-resident planes (generic / team kernel): measured faster there
 template <int FG>
-__device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, uint8_t cur, uint8_t next, int &evals) {
+__device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, int pc, int &evals) {
     bool ch = false;
-    auto strip = [&](int x, int y0, int y1, int sid) {
+    const Marks mk = pass_marks(g, pc);
+    auto strip = [&](int x, int y0, int y1, int) {
         if (y0 >= y1) return;
-        if (!full && g.sflag && (uint8_t)(g.sflag[sid] - cur) > 1) return;   // untouched strip
         int p = pidx(g, y0, x);
         int y = y0;
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
@@ -693,8 +676,7 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, uint8_t c
                     const uint32_t chg = nd ^ dm.c;
                     g.D[p] = nd;
                     dm.c = nd;
-                    stamp_chg(g, p, chg, next);
-                    stamp_strips(g, sid, x, y == y0, y == y1 - 1, chg, next);
+                    stamp_chg(g, p, chg, mk.next);
                     ch = true;
                 }
             }
@@ -707,7 +689,7 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, uint8_t c
         };
         auto fetch = [&](int q, uint32_t &c, uint4 &e0, uint4 &e1) {
             c = g.C[q];
-            if (c && !(full || stamped(g, q, cur))) c = 0;
+            if (c && !(full || stamped(g, mk, q))) c = 0;
             if (c) {
                 const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
                 e0 = ep[0];
@@ -754,7 +736,7 @@ __device__ __forceinline__ void load_slot(const Img &g, uint32_t p, Slot &s) {
 }
 
 template <int FG, bool STAMP>
-__device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t stamp = 0) {
+__device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t M = 0) {
     const uint32_t *u = g.D + s.p - g.S, *m = g.D + s.p, *d = g.D + s.p + g.S;
     Nb dn;
     dn.nw = from_west(u[-1], u[0]);
@@ -767,7 +749,7 @@ __device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t stamp
     dn.se = from_east(d[0], d[1]);
     const uint32_t nd = decide<FG>(s.c, s.in, dn, s.e0, s.e1);
     if (nd != s.d) {
-        if constexpr (STAMP) stamp_chg(g, s.p, nd ^ s.d, stamp);
+        if constexpr (STAMP) stamp_chg(g, s.p, nd ^ s.d, M);
         s.d = nd;
         g.D[s.p] = nd;
         return true;
@@ -859,20 +841,12 @@ struct Stats {
     bool timing;
 };
 
-#ifndef TS_STRIP_FLAGS
-#define TS_STRIP_FLAGS 0
-#endif
-constexpr int kMaxStrips = TS_STRIP_FLAGS ? 4096 : 16;
-
 struct Shared {
     int img;
     int counters[2];
     int bad;
     unsigned long long flips, evals;
-    union {
-        uint8_t sflag[kMaxStrips];
-        long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
-    };
+    long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
 };
 
 // per-team control block in global memory (teams of G > 1 CTAs)
@@ -889,9 +863,9 @@ static_assert(sizeof(TeamCtl) <= kTeamCtlBytes, "kTeamCtlBytes too small");
 // hot planes as 32-bit shared-window addresses (HOT) re-materialised with
 // cvta inside the callee (so accesses compile to LDS/STS), others as pointers.
 struct View {
-    unsigned long long I, D, C, B, dirty, mark;   // shared address (HOT) or pointer bits
-    uint32_t *list, *E, *XS, *R, *K, *A;
-    int H, W, WW, S, plen, org, nblk, hb, dense_min;
+    unsigned long long I, D, C, dirty, mark;   // shared address (HOT) or pointer bits
+    uint32_t *B, *list, *E, *XS, *R, *K, *A;
+    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank;
@@ -913,9 +887,9 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.I = hot_ptr<HOT>(v.I);
     g.D = hot_ptr<HOT>(v.D);
     g.C = hot_ptr<HOT>(v.C);
-    g.B = hot_ptr<HOT>(v.B);
     g.dirty = hot_ptr<HOT>(v.dirty);
     g.mark = reinterpret_cast<uint8_t *>(hot_ptr<HOT>(v.mark));
+    g.B = v.B;
     g.list = v.list;
     g.E = v.E;
     g.XS = v.XS;
@@ -930,6 +904,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.org = v.org;
     g.nblk = v.nblk;
     g.hb = v.hb;
+    g.nstrips = v.nstrips;
     g.dense_min = v.dense_min;
     g.lastmask = v.lastmask;
     // HOT implies a single CTA per image: constants, so team code folds away
@@ -941,14 +916,6 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.err = v.err;
     g.sh = g.G == 1 ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))
                     : reinterpret_cast<Shared *>(v.sh);
-    const int nstrips = v.WW <= g.nthr ? v.nblk * v.WW : v.WW;
-    {
-        const int x = g.tid % v.WW, blk = g.tid / v.WW;
-        g.sx = x;
-        g.sy0 = blk < v.nblk ? blk * v.hb : 0;
-        g.sy1 = blk < v.nblk ? min(v.H, blk * v.hb + v.hb) : 0;
-    }
-    g.sflag = (TS_STRIP_FLAGS && g.G == 1 && nstrips <= kMaxStrips) ? g.sh->sflag : nullptr;
     return g;
 }
 
@@ -1135,8 +1102,8 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
     while (true) {
-        const bool ch = HOT ? dense_pass<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals)
-                            : dense_pass_l2<FG>(g, o.passes == 0, (uint8_t)pc, (uint8_t)(pc + 1), o.evals);
+        const bool ch = HOT ? dense_pass<FG>(g, o.passes == 0, pc, o.evals)
+                            : dense_pass_l2<FG>(g, o.passes == 0, pc, o.evals);
         ++o.passes;
         const bool any = team_any(g, ch, pc);
         ++pc;
@@ -1184,19 +1151,19 @@ __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long 
         return o;
     }
     while (true) {
-        const uint8_t cur_stamp = (uint8_t)pc, next_stamp = (uint8_t)(pc + 1);
+        const Marks mk = pass_marks(g, pc);
         const bool full = o.passes == 0;
         bool ch = false;
-        if (has0 && (full || stamped(g, s0.p, cur_stamp))) {
-            ch = update_slot<FG, true>(g, s0, next_stamp);
+        if (has0 && (full || stamped(g, mk, s0.p))) {
+            ch = update_slot<FG, true>(g, s0, mk.next);
             ++o.evals;
         }
         for (int sl = tid + nthr; sl < n; sl += nthr) {
             const uint32_t p = g.list[sl];
-            if (!full && !stamped(g, (int)p, cur_stamp)) continue;
+            if (!full && !stamped(g, mk, (int)p)) continue;
             Slot s;
             load_slot<FG>(g, p, s);
-            ch |= update_slot<FG, true>(g, s, next_stamp);
+            ch |= update_slot<FG, true>(g, s, mk.next);
             ++o.evals;
         }
         ++o.passes;
@@ -1443,9 +1410,7 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
     for (int q = tid; q < (g.plen + 31) >> 5; q += nthr) g.dirty[q] = 0;
     for (int q = tid; q < (g.plen + 15) >> 4; q += nthr)
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
-    if (g.G == 1) {
-        for (int q = tid; q < kMaxStrips; q += nthr) g.sh->sflag[q] = 0;
-    } else if (tid == 0) {
+    if (g.G > 1 && tid == 0) {
         g.flags[0] = g.flags[1] = g.flags[2] = 0;
     }
     team_sync(g);
@@ -1500,17 +1465,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         v.I = base + 4ull * p.off[B_I];
         v.D = base + 4ull * p.off[B_D];
         v.C = base + 4ull * p.off[B_C];
-        v.B = base + 4ull * p.off[B_B];
         v.dirty = base + 4ull * p.off[B_DIRTY];
         v.mark = base + 4ull * p.off[B_MARK];
     } else {
         v.I = (unsigned long long)buf(B_I);
         v.D = (unsigned long long)buf(B_D);
         v.C = (unsigned long long)buf(B_C);
-        v.B = (unsigned long long)buf(B_B);
         v.dirty = (unsigned long long)buf(B_DIRTY);
         v.mark = (unsigned long long)buf(B_MARK);
     }
+    v.B = buf(B_B);
     v.list = buf(B_LIST);
     v.E = buf(B_E);
     v.XS = buf(B_XS);
@@ -1522,9 +1486,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     v.WW = p.WW;
     v.S = p.stride;
     v.plen = p.plen;
-    v.org = kPadRows * p.stride + 1;
+    v.org = p.pad * p.stride + 1;
     v.nblk = p.nblk;
     v.hb = p.hb;
+    v.nstrips = p.nstrips;
     v.dense_min = p.dense_min;
     v.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
     v.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;

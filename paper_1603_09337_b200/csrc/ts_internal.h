@@ -6,11 +6,12 @@ namespace ts {
 
 // Per-image working buffers of the fused HASF kernel.  Each lives either in
 // the CTA's shared memory or in its private slice of a global workspace
-// (L2-resident); the host places them greedily in this priority order.
-// All planes use the padded layout: kPadRows zero rows above and below the
-// image, one zero word between rows (row stride `stride` >= WW + 1); word
-// (y, x) is at (kPadRows + y) * stride + x + 1; plane length `plen` words.
-constexpr int kPadRows = 16;
+// (L2-resident); the host places them greedily in kPlaceOrder.
+// All planes use the padded layout: `pad` zero rows above and below the image
+// (reads beyond them are clamped to the pad row), one zero word between rows
+// (row stride `stride` >= WW + 1); word (y, x) is at (pad + y) * stride + x + 1;
+// plane length `plen` words.
+constexpr int kPadRows = 1;
 
 // threads per CTA of the fused kernel (host planning must agree)
 #ifndef TS_THREADS
@@ -36,6 +37,10 @@ enum Buf : int {
     B_A,         // avoid constraint plane (optional)                  plen
     B_COUNT
 };
+
+// shared-memory placement priority: the planes every fixpoint evaluation reads
+// with neighbours (I, D), the candidates, the bitmaps; then the rest
+constexpr int kPlaceOrder[B_COUNT] = {B_I, B_D, B_C, B_DIRTY, B_MARK, B_B, B_LIST, B_XS, B_E, B_R, B_K, B_A};
 
 // per-image stats: 0 sweeps, 1 fixpoint passes, 2 engine calls, 3 flips, then
 // thread-0 clock64 cycles: 4 prep (EDT/rank + E passes), 5 fixpoint passes,
@@ -67,6 +72,8 @@ struct KParams {
     const int64_t *prio;    // [n,h,w] (engine modes only)
     int n, H, W, WW, nwords;
     int stride, plen;       // padded layout (see kPadRows)
+    int pad;                // zero rows above / below the image (kPadRows)
+    int nstrips;            // strips = nblk * WW (a thread walks strips tid, tid + nthr, ...)
     int nblk, hb;           // strip mapping: row blocks per word column, rows per block
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
     int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
