@@ -50,7 +50,7 @@ int ts_max_radius(void);
 /* HASF: alternate homotopic cutting and filling at radii 1..r_max.
  * Replaces hasf(img, SmoothingConfig(r_max, adj, keep, avoid)) and smooth(img, r_max)
  * (smoothing.py:187-217).  keep_dev / avoid_dev: [n][h][w] constraint images or
- * NULL.  stats_host: NULL or int64[n*16] receiving per image: sweeps, fixpoint
+ * NULL.  stats_host: NULL or int64[n*32] receiving per image: sweeps, fixpoint
  * passes, engine calls, flips, then SM clock cycles spent in prep (clamped
  * EDT + precedence masks), fixpoint passes, apply+re-examination, in total,
  * and a breakdown by sweep size (fields 8-14; 15 reserved). */
@@ -134,7 +134,8 @@ int ts_selftest_circuit(uint8_t *s84_256_host, uint8_t *s48_256_host);
 int64_t ts_set_smem_budget(int64_t bytes);
 
 /* Tuning: a sweep runs in dense (strip-walk) mode when more than
- * (words / div) words hold candidates (default div = 2).  Returns the previous value. */
+ * (words / div) words hold candidates (default and minimum div = 2).  Returns the
+ * previous value. */
 int32_t ts_set_dense_divisor(int32_t div);
 
 /* Tuning/testing: CTAs cooperating on one image (0 = automatic: teams only for

@@ -13,6 +13,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -210,7 +211,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     pl.threads = threads;
     // strips: one per thread, or two when that leaves a warp's strips on
     // conflicting banks (e.g. 256 threads on 16-word rows: 32-row blocks)
-    if (plan_strips(H, pl.WW, threads * team, pl) > 1 && team == 1) {
+    if (plan_strips(H, pl.WW, threads * team, pl) > 1 && team == 1 && !getenv("TS_ONE_STRIP")) {
         Plan p2 = pl;
         if (plan_strips(H, pl.WW, 2 * threads, p2) == 1) pl = p2;
     }
@@ -230,7 +231,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     size[B_B] = plen;
     size[B_DIRTY] = r4((plen + 31) / 32);
     size[B_MARK] = r4(((plen + 15) / 16) * 4);
-    size[B_LIST] = plen;
+    size[B_LIST] = 2 * plen;   // two compacted re-evaluation lists in dense sweeps
     size[B_E] = 8 * plen;
     size[B_XS] = mode == MODE_HASF ? plen : 0;
     size[B_R] = (long long)pl.slices * plen;
@@ -290,7 +291,7 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         rc = make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, p2, 1, 256, half);
         // (measured: two images per SM pay off only when each thread walks a
         // single strip; with two strips per thread c1 ran 10% slower)
-        if (rc == TS_OK && p2.hot && ((p2.per_sm >= 2 && p2.nstrips <= 256) || knob == 256)) {
+        if (rc == TS_OK && p2.hot && ((p2.per_sm >= 2 && p2.nstrips <= 256) || knob == 256 || getenv("TS_ONE_STRIP"))) {
             pl = p2;
             return TS_OK;
         }
@@ -472,7 +473,9 @@ int ts_max_radius(void) { return kMaxR; }
 
 int64_t ts_set_smem_budget(int64_t bytes) { return g_smem_budget.exchange(bytes < 0 ? 0 : bytes); }
 
-int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 1 ? 1 : div); }
+// >= 2: list sweeps then hold at most nwords / 2 words, which the two
+// compacted lists (half a plane each) rely on
+int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 2 ? 2 : div); }
 
 int32_t ts_set_team_size(int32_t ctas) { return g_team_knob.exchange(ctas < 0 ? 0 : ctas); }
 

@@ -185,6 +185,14 @@ __device__ __forceinline__ void for_strip(const Img &g, F &&f) {
     });
 }
 
+// L1 prefetch through a generic address (a no-op for shared memory)
+#ifndef TS_PF
+#define TS_PF 1
+#endif
+__device__ __forceinline__ void prefetch_l1(const void *a) {
+    if (TS_PF) asm volatile("prefetch.L1 [%0];" ::"l"(a));
+}
+
 // ---- bit packing of uint8 {0,1} images ---------------------------------
 __device__ __forceinline__ uint32_t pack4(uint32_t v) {
     v &= 0x01010101u;
@@ -337,6 +345,8 @@ __device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, boo
     const int SS = g.S;
     for_strip(g, [&](int y, int x, int p) {
         const uint32_t *c = g.I + p;
+        // constraint plane read first: it may live in L2
+        const uint32_t xw = xmode == 1 ? (thin ? g.K[p] : g.A[p]) : (xmode == 2 ? g.XS[p] : 0u);
         // rows beyond the frame read the single zero pad row (-1 or H): all
         // exterior rows are equal, so the disc needs no deeper padding
         const int up = y + 1, dn = g.H - y;
@@ -380,10 +390,9 @@ __device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, boo
         // dil = pixels whose clamped distance is <= r^2
         uint32_t blocked;
         if (thin) {
-            const uint32_t extra = xmode == 1 ? g.K[p] : (xmode == 2 ? g.XS[p] : 0u);
-            blocked = ~dil | extra;
+            blocked = ~dil | xw;   // xw: keep (xmode 1) or XS (xmode 2)
         } else {
-            const uint32_t m = xmode == 1 ? ~g.A[p] : (xmode == 2 ? g.XS[p] : ~0u);
+            const uint32_t m = xmode == 1 ? ~xw : (xmode == 2 ? xw : ~0u);
             blocked = ~(dil & m);
         }
         g.B[p] = blocked | (x == g.WW - 1 ? ~g.lastmask : 0u);
@@ -419,7 +428,10 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
         for (int y = y0; y < y1; ++y, p += g.S) {
             Row3 rd[S];
 #pragma unroll
-            for (int s = 0; s < S; ++s) rd[s] = row3(g.R + (size_t)s * g.plen, p + g.S);
+            for (int s = 0; s < S; ++s) {
+                rd[s] = row3(g.R + (size_t)s * g.plen, p + g.S);
+                prefetch_l1(g.R + (size_t)s * g.plen + p + 2 * g.S);   // next row (L2-resident slices)
+            }
             const Row3 id = row3(g.I, p + g.S);
             const uint32_t bw = g.B[p];
             uint32_t c = 0;
@@ -517,23 +529,30 @@ __device__ __forceinline__ Marks pass_marks(const Img &, int k) { return Marks{(
 __device__ __forceinline__ bool stamped(const Img &g, const Marks &m, int p) { return (uint8_t)(g.mark[p] - m.cur) <= 1; }
 
 // stamp, for re-evaluation in the next pass, the words whose inputs changed
-// when decision bits `chg` of word p flipped: column x in rows y-1..y+1, plus
-// x-1 / x+1 when an edge bit changed
-__device__ __forceinline__ void stamp_chg(const Img &g, int p, uint32_t chg, uint8_t v) {
+// when decision bits `chg` of word p flipped.  A pixel's decision reads the
+// decision of neighbour q only when q precedes it in key order, i.e. (keys
+// are unique) exactly the neighbours in the directions k with E_k(q) == 0; so
+// the E masks of the changed word itself (e0: NW,N,NE,W; e1: E,SW,S,SE) name
+// the neighbour words that can be affected.  `self`: also stamp word p (its
+// own W/E in-word neighbours, when the caller did not resolve them).
+__device__ __forceinline__ void stamp_chg(const Img &g, int p, uint32_t chg, uint4 e0, uint4 e1, uint8_t v,
+                                          bool self) {
     uint8_t *m = g.mark + p;
     const int S = g.S;
-    m[-S] = v;
-    m[0] = v;
-    m[S] = v;
+    const uint32_t lNW = ~e0.x, lN = ~e0.y, lNE = ~e0.z, lW = ~e0.w;   // "that neighbour is later"
+    const uint32_t lE = ~e1.x, lSW = ~e1.y, lS = ~e1.z, lSE = ~e1.w;
+    if (chg & (lN | (lNW & ~1u) | (lNE & 0x7FFFFFFFu))) m[-S] = v;
+    if (chg & (lS | (lSW & ~1u) | (lSE & 0x7FFFFFFFu))) m[S] = v;
+    if (self) m[0] = v;
     if (chg & 1u) {
-        m[-S - 1] = v;
-        m[-1] = v;
-        m[S - 1] = v;
+        if (lNW & 1u) m[-S - 1] = v;
+        if (lW & 1u) m[-1] = v;
+        if (lSW & 1u) m[S - 1] = v;
     }
     if (chg >> 31) {
-        m[-S + 1] = v;
-        m[1] = v;
-        m[S + 1] = v;
+        if (lNE >> 31) m[-S + 1] = v;
+        if (lE >> 31) m[1] = v;
+        if (lSE >> 31) m[S + 1] = v;
     }
 }
 
@@ -549,39 +568,33 @@ __device__ __forceinline__ uint32_t decide(uint32_t c, const Nb &i, const Nb &d,
 // Rows are processed in groups of kDenseBatch: the group's candidate / stamp
 // checks and E loads (from L2 when E does not fit in shared memory) are issued
 // together, then the rows are evaluated in order with the sliding window.
-constexpr int kDenseBatch = 4;
-#ifndef TS_WORD_FIX
-#define TS_WORD_FIX 1
+#ifndef TS_DENSE_BATCH
+#define TS_DENSE_BATCH 4
 #endif
-#ifndef TS_DENSE_SKIP
-#define TS_DENSE_SKIP 1
-#endif
-constexpr bool kDenseSkip = TS_DENSE_SKIP != 0;
+constexpr int kDenseBatch = TS_DENSE_BATCH;
+
 
 template <int FG>
-__device__ __forceinline__ bool dense_pass(const Img &g, bool full, int pc, int &evals) {
+__device__ __forceinline__ bool dense_pass(const Img &g, int pc, int &evals) {
     bool ch = false;
-    const Marks mk = pass_marks(g, pc);
+    const uint8_t next = (uint8_t)(pc + 1);
     auto strip = [&](int x, int y0, int y1, int) {
         if (y0 >= y1) return;
         int p = pidx(g, y0, x);
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
         Row3 du = row3(g.D, p - g.S), dm = row3(g.D, p);
         for (int yb = y0; yb < y1; yb += kDenseBatch) {
+            // the batch's candidates and E masks (L2) are requested together
             uint32_t cb[kDenseBatch];
             uint4 e0b[kDenseBatch], e1b[kDenseBatch];
 #pragma unroll
             for (int j = 0; j < kDenseBatch; ++j) {
                 const int q = p + j * g.S;
-                cb[j] = 0;
-                if (yb + j < y1) {
-                    const uint32_t c = g.C[q];
-                    if (c && (full || stamped(g, mk, q))) {
-                        cb[j] = c;
-                        const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
-                        e0b[j] = ep[0];
-                        e1b[j] = ep[1];
-                    }
+                cb[j] = yb + j < y1 ? g.C[q] : 0u;
+                if (cb[j]) {
+                    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
+                    e0b[j] = ep[0];
+                    e1b[j] = ep[1];
                 }
             }
 #pragma unroll
@@ -589,6 +602,7 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, int pc, int 
                 if (yb + j >= y1) break;
                 const Row3 id = row3(g.I, p + g.S), dd = row3(g.D, p + g.S);
                 const uint32_t c = cb[j];
+                const uint4 e0 = e0b[j], e1 = e1b[j];
                 if (c) {
                     Nb in, dn;
                     in.nw = from_west(iu.l, iu.c);
@@ -607,23 +621,21 @@ __device__ __forceinline__ bool dense_pass(const Img &g, bool full, int pc, int 
                     dn.sw = from_west(dd.l, dd.c);
                     dn.s = dd.c;
                     dn.se = from_east(dd.c, dd.r);
-                    uint32_t nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
-#if TS_WORD_FIX
+                    uint32_t nd = decide<FG>(c, in, dn, e0, e1);
                     // resolve chains inside the word now: re-decide with the
                     // word's own new decisions as its W/E neighbours
                     for (uint32_t pd = dm.c; nd != pd;) {
                         pd = nd;
                         dn.w = from_west(dm.l, nd);
                         dn.e = from_east(nd, dm.r);
-                        nd = decide<FG>(c, in, dn, e0b[j], e1b[j]);
+                        nd = decide<FG>(c, in, dn, e0, e1);
                     }
-#endif
                     ++evals;
                     if (nd != dm.c) {
                         const uint32_t chg = nd ^ dm.c;
                         g.D[p] = nd;
                         dm.c = nd;   // the next row sees this update (Gauss-Seidel down the strip)
-                        stamp_chg(g, p, chg, mk.next);
+                        stamp_chg(g, p, chg, e0, e1, next, false);
                         ch = true;
                     }
                 }
@@ -676,7 +688,7 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, int pc, i
                     const uint32_t chg = nd ^ dm.c;
                     g.D[p] = nd;
                     dm.c = nd;
-                    stamp_chg(g, p, chg, mk.next);
+                    stamp_chg(g, p, chg, e0, e1, mk.next, true);
                     ch = true;
                 }
             }
@@ -749,7 +761,7 @@ __device__ __forceinline__ bool update_slot(const Img &g, Slot &s, uint8_t M = 0
     dn.se = from_east(d[0], d[1]);
     const uint32_t nd = decide<FG>(s.c, s.in, dn, s.e0, s.e1);
     if (nd != s.d) {
-        if constexpr (STAMP) stamp_chg(g, s.p, nd ^ s.d, M);
+        if constexpr (STAMP) stamp_chg(g, s.p, nd ^ s.d, s.e0, s.e1, M, true);
         s.d = nd;
         g.D[s.p] = nd;
         return true;
@@ -847,6 +859,10 @@ struct Shared {
     int bad;
     unsigned long long flips, evals;
     long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
+    int lcount[2];       // lengths of the two compacted re-evaluation lists (dense sweeps)
+    long long dtime[4];  // stats: dense pass-1 / collect / list-pass cycles, listed words
+    long long sstat[4];  // stats: list sweeps (33..512 words) count / cycles, (> 512) count / cycles
+    long long bstat[4];  // stats, list sweeps > 512 words: list-build / sweep / re-examination cycles, list builds
 };
 
 // per-team control block in global memory (teams of G > 1 CTAs)
@@ -1096,22 +1112,223 @@ __device__ __noinline__ TinyOut tiny_sweeps(const View v, int t, int cur, long l
     return o;
 }
 
-// dense sweep: worklist passes over the strips, then apply (all threads)
-template <int FG, bool HOT>
-__device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int pc0) {
+// ---- compacted re-evaluation passes (dense sweeps after their first pass) --
+// After the strip-walk pass only the words stamped by a changed neighbour
+// decision need evaluating -- a few percent of the image, scattered, so a
+// strip walk would run its warps mostly idle.  Instead the stamped candidate
+// words are gathered into a list and evaluated one word per thread.  A pass
+// whose changes stamp no candidate word reached the fixpoint (every
+// candidate's inputs are unchanged), so an empty list ends the sweep.
+
+// words stamped `v` holding candidates -> list (all team threads; *counter
+// zeroed by the caller before a barrier)
+__device__ __forceinline__ void collect_stamped(const Img &g, uint8_t v, uint32_t *list, int *counter) {
+    const int nchunk = (g.plen + 15) >> 4;   // 16 stamps per uint4
+    const uint32_t vv = 0x01010101u * v;
+    const int lane = threadIdx.x & 31;
+    for (int c0 = g.tid - lane; c0 < nchunk; c0 += g.nthr) {   // warp-uniform trip count
+        const int ch = c0 + lane;
+        uint32_t valid = 0;
+        if (ch < nchunk) {
+            const uint4 m = reinterpret_cast<const uint4 *>(g.mark)[ch];
+            // one bit per matching stamp byte: byte b of word k -> bit 4k + b
+            const uint32_t h = ((__vcmpeq4(m.x, vv) & 0x01010101u) * 0x10204080u) >> 28 |
+                               (((__vcmpeq4(m.y, vv) & 0x01010101u) * 0x10204080u) >> 28) << 4 |
+                               (((__vcmpeq4(m.z, vv) & 0x01010101u) * 0x10204080u) >> 28) << 8 |
+                               (((__vcmpeq4(m.w, vv) & 0x01010101u) * 0x10204080u) >> 28) << 12;
+            for (uint32_t t = h; t; t &= t - 1) {
+                const int b = __ffs(t) - 1;
+                if (ch * 16 + b < g.plen && g.C[ch * 16 + b]) valid |= 1u << b;
+            }
+        }
+        const int cnt = __popc(valid);
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int base = 0;
+        if (lane == 31) base = atomicAdd(counter, tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+        for (uint32_t t = valid; t; t &= t - 1) list[base++] = (uint32_t)(ch * 16 + __ffs(t) - 1);
+    }
+}
+
+// one listed word's evaluation: inputs, then the word-fix solve, then commit
+struct WordEval {
+    int p;
+    Nb in, dn;       // image neighbours; decision neighbours (W/E from the word itself)
+    uint4 e0, e1;    // E masks
+    uint32_t c, ml, mr, old;
+};
+
+__device__ __forceinline__ void load_eval(const Img &g, int p, WordEval &w) {
+    w.p = p;
+    w.in = nbrs(g.I, g, p);
+    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)p * 8);
+    w.e0 = ep[0];
+    w.e1 = ep[1];
+    w.c = g.C[p];
+    const uint32_t *u = g.D + p - g.S, *m = g.D + p, *d = g.D + p + g.S;
+    w.dn.nw = from_west(u[-1], u[0]);
+    w.dn.n = u[0];
+    w.dn.ne = from_east(u[0], u[1]);
+    w.dn.sw = from_west(d[-1], d[0]);
+    w.dn.s = d[0];
+    w.dn.se = from_east(d[0], d[1]);
+    w.ml = m[-1];
+    w.mr = m[1];
+    w.old = m[0];
+}
+
+// decisions of the word with its in-word chains resolved (word fix)
+template <int FG>
+__device__ __forceinline__ uint32_t solve_eval(WordEval &w) {
+    uint32_t nd = w.old;
+    for (uint32_t pd = ~w.old; nd != pd;) {
+        pd = nd;
+        w.dn.w = from_west(w.ml, nd);
+        w.dn.e = from_east(nd, w.mr);
+        nd = decide<FG>(w.c, w.in, w.dn, w.e0, w.e1);
+    }
+    return nd;
+}
+
+__device__ __forceinline__ bool commit_eval(const Img &g, const WordEval &w, uint32_t nd, uint8_t next) {
+    if (nd == w.old) return false;
+    g.D[w.p] = nd;
+    stamp_chg(g, w.p, nd ^ w.old, w.e0, w.e1, next, false);
+    return true;
+}
+
+// re-evaluate the listed words (two per thread at a time, so the loads of both
+// are in flight together); changes stamp the affected neighbour words `next`
+template <int FG>
+__device__ __forceinline__ bool list_pass(const Img &g, const uint32_t *list, int n, uint8_t next, int &evals) {
+    bool ch = false;
+    const int nthr = g.nthr;
+#ifndef TS_LIST2
+#define TS_LIST2 0
+#endif
+    if (!TS_LIST2) {
+        for (int sl = g.tid; sl < n; sl += nthr) {
+            WordEval a;
+            load_eval(g, (int)list[sl], a);
+            ch |= commit_eval(g, a, solve_eval<FG>(a), next);
+            ++evals;
+        }
+        return ch;
+    }
+    for (int sl = g.tid; sl < n; sl += 2 * nthr) {
+        const bool two = sl + nthr < n;
+        WordEval a, b;
+        load_eval(g, (int)list[sl], a);
+        if (two) load_eval(g, (int)list[sl + nthr], b);
+        const uint32_t na = solve_eval<FG>(a);
+        const uint32_t nb = two ? solve_eval<FG>(b) : 0u;
+        ch |= commit_eval(g, a, na, next);
+        if (two) ch |= commit_eval(g, b, nb, next);
+        evals += two ? 2 : 1;
+    }
+    return ch;
+}
+
+// sweep-list words stamped `v` -> list (the sweep's candidates are all listed)
+__device__ __forceinline__ void filter_stamped(const Img &g, const uint32_t *from, int n, uint8_t v, uint32_t *list,
+                                               int *counter) {
+    const int lane = threadIdx.x & 31;
+    for (int s0 = g.tid - lane; s0 < n; s0 += g.nthr) {   // warp-uniform trip count
+        const int sl = s0 + lane;
+        const uint32_t p = sl < n ? from[sl] : 0u;
+        const bool has = sl < n && g.mark[p] == v;
+        const unsigned m = __ballot_sync(0xffffffffu, has);
+        if (m == 0) continue;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(counter, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (has) list[base + __popc(m & ((1u << lane) - 1u))] = p;
+    }
+}
+
+// list sweep (> 32 listed words): one pass over the sweep list, then
+// compacted passes over the stamped words until none is stamped; then apply
+template <int FG>
+__device__ __forceinline__ SweepOut list_sweep(const Img &g, int n, long long cap, int pc0) {
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
-    while (true) {
-        const bool ch = HOT ? dense_pass<FG>(g, o.passes == 0, pc, o.evals)
-                            : dense_pass_l2<FG>(g, o.passes == 0, pc, o.evals);
-        ++o.passes;
-        const bool any = team_any(g, ch, pc);
-        ++pc;
-        if (!any) break;
+    Shared &sh = *g.sh;
+    uint32_t *lists[2] = {g.list + g.plen, g.list + g.plen + g.plen / 2};   // each >= nwords / 2 >= n
+    if (g.tid == 0) sh.lcount[1] = 0;
+    list_pass<FG>(g, g.list, n, (uint8_t)(pc + 1), o.evals);
+    ++o.passes;
+    ++pc;
+    for (int k = 1;; k ^= 1) {
+        team_sync(g);
+        filter_stamped(g, g.list, n, (uint8_t)pc, lists[k], &sh.lcount[k]);
+        if (g.tid == 0) sh.lcount[k ^ 1] = 0;
+        team_sync(g);
+        const int m = *reinterpret_cast<volatile int *>(&sh.lcount[k]);
+        if (m == 0) break;
         if (o.passes > cap) {
             o.bad = true;
             break;
         }
+        list_pass<FG>(g, lists[k], m, (uint8_t)(pc + 1), o.evals);
+        ++o.passes;
+        ++pc;
+    }
+    for (int sl = g.tid; sl < n; sl += g.nthr) {
+        const int p = (int)g.list[sl];
+        o.flips += apply_word(g, p, g.D[p]);
+    }
+    return o;
+}
+
+// dense sweep: one strip-walk pass, then compacted passes until no candidate
+// word is stamped; then apply (all threads)
+template <int FG, bool HOT>
+__device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int pc0, bool timing) {
+    SweepOut o{0, 0, 0, false};
+    int pc = pc0;
+    Shared &sh = *g.sh;
+    uint32_t *lists[2] = {g.list, g.list + g.plen};
+    const bool tm = timing && g.tid == 0;
+    long long t0 = tm ? clock64() : 0;
+    if (g.tid == 0) sh.lcount[1] = 0;
+    if (HOT)
+        dense_pass<FG>(g, pc, o.evals);
+    else
+        dense_pass_l2<FG>(g, true, pc, o.evals);
+    ++o.passes;
+    ++pc;
+    for (int k = 1;; k ^= 1) {
+        team_sync(g);   // stamps of the previous pass complete
+        if (tm) {
+            const long long t1 = clock64();
+            sh.dtime[o.passes == 1 ? 0 : 2] += t1 - t0;
+            t0 = t1;
+        }
+        collect_stamped(g, (uint8_t)pc, lists[k], &sh.lcount[k]);
+        if (g.tid == 0) sh.lcount[k ^ 1] = 0;   // the list after next (its last reader finished before the sync)
+        team_sync(g);
+        const int n = *reinterpret_cast<volatile int *>(&sh.lcount[k]);
+        if (tm) {
+            const long long t1 = clock64();
+            sh.dtime[1] += t1 - t0;
+            sh.dtime[3] += n;
+            t0 = t1;
+        }
+        if (n == 0) break;
+        if (o.passes > cap) {
+            o.bad = true;
+            break;
+        }
+        list_pass<FG>(g, lists[k], n, (uint8_t)(pc + 1), o.evals);
+        ++o.passes;
+        ++pc;
     }
     for_strip(g, [&](int y, int x, int p) {
         const uint32_t dw = g.D[p];
@@ -1127,9 +1344,9 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
 // sparse sweep over the n listed words, then apply (all threads)
 template <int FG>
 __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long cap, int pc0) {
-    const int tid = g.tid, warp = tid >> 5, nthr = g.nthr;
+    if (n > 32) return list_sweep<FG>(g, n, cap, pc0);
+    const int tid = g.tid, warp = tid >> 5;
     SweepOut o{0, 0, 0, false};
-    int pc = pc0;
     Slot s0;
     const bool has0 = tid < n;
     if (has0) load_slot<FG>(g, g.list[tid], s0);
@@ -1148,39 +1365,21 @@ __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long 
             }
             if (has0) o.flips += apply_word(g, s0.p, s0.d);
         }
-        return o;
-    }
-    while (true) {
-        const Marks mk = pass_marks(g, pc);
-        const bool full = o.passes == 0;
-        bool ch = false;
-        if (has0 && (full || stamped(g, mk, s0.p))) {
-            ch = update_slot<FG, true>(g, s0, mk.next);
-            ++o.evals;
-        }
-        for (int sl = tid + nthr; sl < n; sl += nthr) {
-            const uint32_t p = g.list[sl];
-            if (!full && !stamped(g, mk, (int)p)) continue;
-            Slot s;
-            load_slot<FG>(g, p, s);
-            ch |= update_slot<FG, true>(g, s, mk.next);
-            ++o.evals;
-        }
-        ++o.passes;
-        const bool any = team_any(g, ch, pc);
-        ++pc;
-        if (!any) break;
-        if (o.passes > cap) {
-            o.bad = true;
-            break;
-        }
-    }
-    if (has0) o.flips += apply_word(g, s0.p, s0.d);
-    for (int sl = tid + nthr; sl < n; sl += nthr) {
-        const int p = (int)g.list[sl];
-        o.flips += apply_word(g, p, g.D[p]);
     }
     return o;
+}
+
+// the sweeps as separate functions: each gets its own register allocation
+template <int FG, bool HOT>
+__device__ __noinline__ SweepOut dense_sweep_nl(const View v, long long cap, int pc, bool timing) {
+    const Img g = make_img<HOT>(v);
+    return dense_sweep<FG, HOT>(g, cap, pc, timing);
+}
+
+template <int FG, bool HOT>
+__device__ __noinline__ SweepOut sparse_sweep_nl(const View v, int n, long long cap, int pc) {
+    const Img g = make_img<HOT>(v);
+    return sparse_sweep<FG>(g, n, cap, pc);
 }
 
 template <int FG>
@@ -1254,7 +1453,12 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
             build_list(g, &sh.counters[cur ^ 1]);
             team_sync(g);
             list_ok = true;
+            if (st.timing && tid == 0 && n > 512) {
+                sh.bstat[0] += clock64() - tj0;
+                sh.bstat[3] += 1;
+            }
         }
+        const long long tjb = st.timing ? clock64() : 0;
         if (tiny) {
             long long budget = sweep_cap - sweeps;
             if (max_sweeps >= 0) budget = min(budget, max_sweeps - sweeps);
@@ -1291,9 +1495,9 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
         }
         SweepOut o;
         if (dense)
-            o = dense_sweep<FG, HOT>(g, cap, pc);
+            o = dense_sweep_nl<FG, HOT>(v, cap, pc, st.timing);
         else
-            o = sparse_sweep<FG>(g, n, cap, pc);
+            o = sparse_sweep_nl<FG, HOT>(v, n, cap, pc);
         if (tid == 0) {
             sh.bad = o.bad ? 1 : 0;
             sh.counters[cur ^ 1] = 0;
@@ -1333,6 +1537,14 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
                 st.cyc_tiny += tj1 - tj0;
                 st.n_tiny += 1;
                 st.pass_tiny += o.passes;
+            } else if (tid == 0) {
+                const int b = n <= 512 ? 0 : 2;
+                sh.sstat[b] += 1;
+                sh.sstat[b + 1] += tj2 - tj0;
+                if (n > 512) {
+                    sh.bstat[1] += tj1 - tjb;
+                    sh.bstat[2] += tj2 - tj1;
+                }
             }
         }
     }
@@ -1513,6 +1725,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.counters[0] = 0;
             sh.flips = 0;
             sh.evals = 0;
+            sh.dtime[0] = sh.dtime[1] = sh.dtime[2] = sh.dtime[3] = 0;
+            sh.sstat[0] = sh.sstat[1] = sh.sstat[2] = sh.sstat[3] = 0;
+            sh.bstat[0] = sh.bstat[1] = sh.bstat[2] = sh.bstat[3] = 0;
         }
         load_image_nl<HOT>(v, &p, pix);
         team_sync(gk);
@@ -1559,6 +1774,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sp[13] = st.pass_dense;
             sp[14] = st.cyc_rank;
             sp[15] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.evals);
+            for (int k = 0; k < 4; ++k) {
+                sp[16 + k] = *reinterpret_cast<volatile long long *>(&sh.sstat[k]);
+                sp[20 + k] = *reinterpret_cast<volatile long long *>(&sh.dtime[k]);
+                sp[24 + k] = *reinterpret_cast<volatile long long *>(&sh.bstat[k]);
+            }
         }
         team_sync(gk);
     }

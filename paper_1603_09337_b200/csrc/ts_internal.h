@@ -47,7 +47,11 @@ constexpr int kPlaceOrder[B_COUNT] = {B_I, B_D, B_C, B_DIRTY, B_MARK, B_B, B_LIS
 // 6 apply+rebuild, 7 whole image (incl. pack/unpack); 8-10 cycles / sweeps /
 // passes of tiny sweeps (<= 32 words), 11-13 the same for dense sweeps
 // (> one word per thread), 14 cycles of the clamped-EDT part of prep
-constexpr int kStatFields = 16;
+// 16-19 list sweeps of 33..512 words: count, cycles (incl. re-examination),
+// of > 512 words: count, cycles; 20-23 dense sweeps: cycles of the strip-walk pass, of the list collection
+// (incl. barriers), of the compacted passes; listed words; 24-27 list sweeps
+// of > 512 words: list-build, sweep, re-examination cycles, list builds
+constexpr int kStatFields = 32;
 
 enum Mode : int { MODE_HASF = 0, MODE_THIN = 1, MODE_THICKEN = 2 };
 

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--dense-div", type=int, default=0)
     ap.add_argument("--team", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--verify", type=int, default=0, help="images checked bit-exact vs the oracle")
     args = ap.parse_args()
     import torch
     import paper_1603_09337_b200 as P
@@ -55,13 +56,24 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         res[f"ms_{i}"] = e0.elapsed_time(e1)
+    res["ms_min"] = min(res[f"ms_{i}"] for i in range(args.repeat))
+    if args.verify:
+        import oracle as O
+        got = out.cpu().numpy()
+        host = imgs.cpu().numpy()
+        bad = [i for i in range(min(args.verify, args.n))
+               if not np.array_equal(got[i], O.hasf(host[i], cfg.r_max, cfg.fg))]
+        res["verify_bad"] = bad
     if args.stats:
         m = st.mean(axis=0)
         res.update({"sweeps": m[0], "passes": m[1], "calls": m[2], "flips": m[3],
                     "cyc_prep": m[4], "cyc_jacobi": m[5], "cyc_update": m[6], "cyc_total": m[7],
                     "cyc_total_max": int(st[:, 7].max()), "cyc_total_min": int(st[:, 7].min()),
                     "cyc_tiny": m[8], "n_tiny": m[9], "pass_tiny": m[10], "cyc_dense": m[11], "n_dense": m[12],
-                    "pass_dense": m[13], "cyc_rank": m[14], "evals": m[15]})
+                    "pass_dense": m[13], "cyc_rank": m[14], "evals": m[15],
+                                        "n_sp_small": m[16], "cyc_sp_small": m[17], "n_sp_big": m[18], "cyc_sp_big": m[19],
+                    "b_build": m[24], "b_sweep": m[25], "b_rebuild": m[26], "n_build": m[27],
+                    "cyc_dpass1": m[20], "cyc_dcollect": m[21], "cyc_dlist": m[22], "d_listed": m[23]})
     print(json.dumps(res, default=float))
 
 
