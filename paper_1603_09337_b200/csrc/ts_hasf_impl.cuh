@@ -433,14 +433,14 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
                 prefetch_l1(g.R + (size_t)s * g.plen + p + 2 * g.S);   // next row (L2-resident slices)
             }
             const Row3 id = row3(g.I, p + g.S);
-            const uint32_t bw = g.B[p];
+            // E is read only for words holding candidates in some sweep of this
+            // engine call, and those lie inside the unblocked target pixels
+            // (flips never create target pixels): skip the rest
+            const uint32_t pre = (t ? im.c : ~im.c) & ~g.B[p];
             uint32_t c = 0;
-            if (~bw) {
-                const uint32_t pre = (t ? im.c : ~im.c) & ~bw;
-                if (pre)
-                    c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r),
-                                              from_west(im.l, im.c), from_east(im.c, im.r), from_west(id.l, id.c),
-                                              id.c, from_east(id.c, id.r));
+            if (pre) {
+                c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
+                                          from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
                 uint32_t lt[8], eq[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -792,6 +792,50 @@ __device__ __forceinline__ unsigned apply_word(const Img &g, int p, uint32_t dw)
     return __popc(dw);
 }
 
+// re-examination after a list sweep: the dirty bitmap is compacted into a
+// word list (thread per bitmap word, warp prefix sums), then every listed word
+// is re-examined by one thread -- full lanes instead of a warp per bitmap word
+template <int FG>
+__device__ __forceinline__ void rebuild_compact(const Img &g, int t, uint32_t *dl, int *dcount, int *counter) {
+    const int lane = threadIdx.x & 31;
+    const int nq = (g.plen + 31) >> 5;
+    for (int q0 = g.tid - lane; q0 < nq; q0 += g.nthr) {   // warp-uniform trip count
+        const int q = q0 + lane;
+        uint32_t bits = 0;
+        if (q < nq) {
+            bits = g.dirty[q];
+            if (bits) g.dirty[q] = 0;
+        }
+        const int cnt = __popc(bits);
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int base = 0;
+        if (lane == 31) base = atomicAdd(dcount, tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+        for (; bits; bits &= bits - 1) dl[base++] = (uint32_t)(q * 32 + __ffs(bits) - 1);
+    }
+    team_sync(g);
+    const int nd = *reinterpret_cast<volatile int *>(dcount);
+    for (int s0 = g.tid - lane; s0 < nd; s0 += g.nthr) {   // warp-uniform trip count
+        const int sl = s0 + lane;
+        uint32_t c = 0;
+        int p = 0;
+        if (sl < nd) {
+            p = (int)dl[sl];
+            c = cand_word<FG>(g, p, t);
+            g.C[p] = c;
+            g.D[p] = c;
+        }
+        append(c != 0, (uint32_t)p, g.list, counter);
+    }
+}
+
 // re-examine every dirty word (warp per 32-word bitmap group, lane = word)
 template <int FG>
 __device__ __forceinline__ void rebuild_sparse(const Img &g, int t, int *counter) {
@@ -860,6 +904,7 @@ struct Shared {
     unsigned long long flips, evals;
     long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
     int lcount[2];       // lengths of the two compacted re-evaluation lists (dense sweeps)
+    int dcount;          // dirty words listed for re-examination after a list sweep
     long long dtime[4];  // stats: dense pass-1 / collect / list-pass cycles, listed words
     long long sstat[4];  // stats: list sweeps (33..512 words) count / cycles, (> 512) count / cycles
     long long bstat[4];  // stats, list sweeps > 512 words: list-build / sweep / re-examination cycles, list builds
@@ -1261,7 +1306,10 @@ __device__ __forceinline__ SweepOut list_sweep(const Img &g, int n, long long ca
     int pc = pc0;
     Shared &sh = *g.sh;
     uint32_t *lists[2] = {g.list + g.plen, g.list + g.plen + g.plen / 2};   // each >= nwords / 2 >= n
-    if (g.tid == 0) sh.lcount[1] = 0;
+    if (g.tid == 0) {
+        sh.lcount[1] = 0;
+        sh.dcount = 0;
+    }
     list_pass<FG>(g, g.list, n, (uint8_t)(pc + 1), o.evals);
     ++o.passes;
     ++pc;
@@ -1382,10 +1430,15 @@ __device__ __noinline__ SweepOut sparse_sweep_nl(const View v, int n, long long 
     return sparse_sweep<FG>(g, n, cap, pc);
 }
 
+// re-examination after a sweep: all words (dense), the compacted dirty words
+// (list sweeps; the compacted lists' space is free again) or the dirty bitmap
+// by warps (a team's warp-only sweeps)
 template <int FG>
-__device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int t, int *counter) {
+__device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int n, int t, int *counter) {
     if (dense)
         rebuild_dense<FG>(g, t, counter);
+    else if (n > 32)
+        rebuild_compact<FG>(g, t, g.list + g.plen, &g.sh->dcount, counter);
     else
         rebuild_sparse<FG>(g, t, counter);
 }
@@ -1520,7 +1573,7 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
         }
         const long long tj1 = st.timing ? clock64() : 0;
         cur ^= 1;
-        rebuild_any<FG>(g, dense, t, &sh.counters[cur]);
+        rebuild_any<FG>(g, dense, n, t, &sh.counters[cur]);
         list_ok = !dense;
         team_sync(g);
         ++sweeps;
