@@ -204,7 +204,7 @@ constexpr int kBigThreads = TS_BIG_THREADS;   // threads per CTA of the one-CTA-
 // one fixed flavour: `threads` per CTA, `team` CTAs per image, shared-memory
 // budget `budget_cap` bytes per CTA (<= 0: device maximum)
 int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team,
-                    int threads, long long budget_cap) {
+                    int threads, long long budget_cap, bool skip_fused = false) {
     pl.WW = (W + 31) / 32;
     if (H >= (1 << 20) || pl.WW >= (1 << 16))
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");
@@ -234,7 +234,11 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     size[B_LIST] = 2 * plen;   // two compacted re-evaluation lists in dense sweeps
     size[B_E] = 8 * plen;
     size[B_XS] = mode == MODE_HASF ? plen : 0;
-    size[B_R] = (long long)pl.slices * plen;
+    // the fused prep + E-pass (one strip per thread, rows of <= 32 words that
+    // tile a warp, r <= 8) keeps the rank slices in registers: no R planes
+    const bool fused = mode == MODE_HASF && team == 1 && pl.nstrips <= threads && 32 % pl.WW == 0 &&
+                       r_last <= kFusedMaxR && !skip_fused;
+    size[B_R] = fused ? 0 : (long long)pl.slices * plen;
     size[B_K] = (mode == MODE_HASF && has_k) ? plen : 0;
     size[B_A] = (mode == MODE_HASF && has_a) ? plen : 0;
 
@@ -268,6 +272,8 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     const uint32_t hot_mask =
         (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_DIRTY) | (1u << B_MARK);
     pl.hot = (pl.mask & hot_mask) == hot_mask;
+    if (fused && !pl.hot)   // the fused path runs only with the hot placement: plan the R planes
+        return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, budget_cap, true);
     pl.team = team;
     int blocks = 0;
     if (threads == 256 && !pl.hot) return fail(TS_ERR_UNSUPPORTED, "256-thread flavour needs the hot placement");

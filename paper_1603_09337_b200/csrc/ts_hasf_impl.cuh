@@ -336,69 +336,78 @@ struct Lev {
 // (the zero pads and padding bits make ~I the exterior seed automatically)
 // xmode (thin) : 0 -> F = P > r^2 ; 1 -> | keep ; 2 -> | XS
 // xmode (thick): 0 -> V = D <= r^2 ; 1 -> & ~avoid ; 2 -> & XS
+// rank slices rs[] and blocked bits of word (y, x) (padded index p)
 template <int R>
-__device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, bool save_xs) {
+__device__ __forceinline__ uint32_t rank_word(const Img &g, int y, int x, int p, bool thin, int xmode,
+                                              uint32_t (&rs)[Lev<R>::S]) {
     using LV = Lev<R>;
     constexpr int L = LV::L;
     constexpr int S = LV::S;
     const uint32_t inv = thin ? ~0u : 0u;
     const int SS = g.S;
-    for_strip(g, [&](int y, int x, int p) {
-        const uint32_t *c = g.I + p;
-        // constraint plane read first: it may live in L2
-        const uint32_t xw = xmode == 1 ? (thin ? g.K[p] : g.A[p]) : (xmode == 2 ? g.XS[p] : 0u);
-        // rows beyond the frame read the single zero pad row (-1 or H): all
-        // exterior rows are equal, so the disc needs no deeper padding
-        const int up = y + 1, dn = g.H - y;
-        uint32_t V[R + 1][3];
-        V[0][0] = c[-1] ^ inv;
-        V[0][1] = c[0] ^ inv;
-        V[0][2] = c[1] ^ inv;
+    const uint32_t *c = g.I + p;
+    // constraint plane read first: it may live in L2
+    const uint32_t xw = xmode == 1 ? (thin ? g.K[p] : g.A[p]) : (xmode == 2 ? g.XS[p] : 0u);
+    // rows beyond the frame read the single zero pad row (-1 or H): all
+    // exterior rows are equal, so the disc needs no deeper padding
+    const int up = y + 1, dn = g.H - y;
+    uint32_t V[R + 1][3];
+    V[0][0] = c[-1] ^ inv;
+    V[0][1] = c[0] ^ inv;
+    V[0][2] = c[1] ^ inv;
 #pragma unroll
-        for (int k = 1; k <= R; ++k) {
-            const uint32_t *a = c - min(k, up) * SS, *b = c + min(k, dn) * SS;
-            V[k][0] = V[k - 1][0] | (a[-1] ^ inv) | (b[-1] ^ inv);
-            V[k][1] = V[k - 1][1] | (a[0] ^ inv) | (b[0] ^ inv);
-            V[k][2] = V[k - 1][2] | (a[1] ^ inv) | (b[1] ^ inv);
-        }
-        uint32_t dil = 0, prev = 0;
-        uint32_t rs[S];
+    for (int k = 1; k <= R; ++k) {
+        const uint32_t *a = c - min(k, up) * SS, *b = c + min(k, dn) * SS;
+        V[k][0] = V[k - 1][0] | (a[-1] ^ inv) | (b[-1] ^ inv);
+        V[k][1] = V[k - 1][1] | (a[0] ^ inv) | (b[0] ^ inv);
+        V[k][2] = V[k - 1][2] | (a[1] ^ inv) | (b[1] ^ inv);
+    }
+    uint32_t dil = 0, prev = 0;
 #pragma unroll
-        for (int s = 0; s < S; ++s) rs[s] = 0;
-        static_for<L>([&](auto ic) {
-            constexpr int i = decltype(ic)::value;
-            static_for<2 * R + 1>([&](auto jc) {
-                constexpr int dx = decltype(jc)::value - R;
-                constexpr int k = LV::kat(i, dx);
-                constexpr int kp = (i == 0) ? -1 : LV::kat(i - 1, dx);
-                if constexpr (k >= 0 && k != kp) {
-                    if constexpr (dx == 0)
-                        dil |= V[k][1];
-                    else if constexpr (dx > 0)
-                        dil |= __funnelshift_r(V[k][1], V[k][2], dx);
-                    else
-                        dil |= __funnelshift_l(V[k][0], V[k][1], -dx);
-                }
-            });
-            const uint32_t newly = dil & ~prev;
-            static_for<S>([&](auto sc) {
-                constexpr int s = decltype(sc)::value;
-                if constexpr (((i >> s) & 1) != 0) rs[s] |= newly;
-            });
-            prev = dil;
+    for (int s = 0; s < S; ++s) rs[s] = 0;
+    static_for<L>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        static_for<2 * R + 1>([&](auto jc) {
+            constexpr int dx = decltype(jc)::value - R;
+            constexpr int k = LV::kat(i, dx);
+            constexpr int kp = (i == 0) ? -1 : LV::kat(i - 1, dx);
+            if constexpr (k >= 0 && k != kp) {
+                if constexpr (dx == 0)
+                    dil |= V[k][1];
+                else if constexpr (dx > 0)
+                    dil |= __funnelshift_r(V[k][1], V[k][2], dx);
+                else
+                    dil |= __funnelshift_l(V[k][0], V[k][1], -dx);
+            }
         });
-        // dil = pixels whose clamped distance is <= r^2
-        uint32_t blocked;
-        if (thin) {
-            blocked = ~dil | xw;   // xw: keep (xmode 1) or XS (xmode 2)
-        } else {
-            const uint32_t m = xmode == 1 ? ~xw : (xmode == 2 ? xw : ~0u);
-            blocked = ~(dil & m);
-        }
-        g.B[p] = blocked | (x == g.WW - 1 ? ~g.lastmask : 0u);
+        const uint32_t newly = dil & ~prev;
+        static_for<S>([&](auto sc) {
+            constexpr int s = decltype(sc)::value;
+            if constexpr (((i >> s) & 1) != 0) rs[s] |= newly;
+        });
+        prev = dil;
+    });
+    // dil = pixels whose clamped distance is <= r^2
+    uint32_t blocked;
+    if (thin) {
+        blocked = ~dil | xw;   // xw: keep (xmode 1) or XS (xmode 2)
+    } else {
+        const uint32_t m = xmode == 1 ? ~xw : (xmode == 2 ? xw : ~0u);
+        blocked = ~(dil & m);
+    }
+    return blocked | (x == g.WW - 1 ? ~g.lastmask : 0u);
+}
+
+template <int R>
+__device__ __forceinline__ int prep_rank(const Img &g, bool thin, int xmode, bool save_xs) {
+    constexpr int S = Lev<R>::S;
+    for_strip(g, [&](int y, int x, int p) {
+        uint32_t rs[S];
+        const uint32_t xs = g.I[p];
+        g.B[p] = rank_word<R>(g, y, x, p, thin, xmode, rs);
 #pragma unroll
         for (int s = 0; s < S; ++s) g.R[(size_t)s * g.plen + p] = rs[s];
-        if (save_xs) g.XS[p] = c[0];
+        if (save_xs) g.XS[p] = xs;
     });
     return S;
 }
@@ -408,6 +417,34 @@ static_assert(kMaxR == 16, "prep_dispatch covers radii 1..16");
 __device__ __forceinline__ void cmp_step(uint32_t &lt, uint32_t &eq, uint32_t nb, uint32_t own) {
     lt |= eq & ~nb & own;   // neighbour < own at the first differing slice
     eq &= ~(nb ^ own);
+}
+
+// E masks of word p from the rank slices of its 3x3 word neighbourhood
+// (bit-sliced comparator, most significant slice first), stored interleaved
+template <int S>
+__device__ __forceinline__ void store_e(const Img &g, int p, const Row3 (&ru)[S], const Row3 (&rm)[S],
+                                        const Row3 (&rd)[S]) {
+    uint32_t lt[8], eq[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        lt[k] = 0;
+        eq[k] = ~0u;
+    }
+#pragma unroll
+    for (int s = S - 1; s >= 0; --s) {
+        const uint32_t own = rm[s].c;
+        cmp_step(lt[0], eq[0], from_west(ru[s].l, ru[s].c), own);
+        cmp_step(lt[1], eq[1], ru[s].c, own);
+        cmp_step(lt[2], eq[2], from_east(ru[s].c, ru[s].r), own);
+        cmp_step(lt[3], eq[3], from_west(rm[s].l, rm[s].c), own);
+        cmp_step(lt[4], eq[4], from_east(rm[s].c, rm[s].r), own);
+        cmp_step(lt[5], eq[5], from_west(rd[s].l, rd[s].c), own);
+        cmp_step(lt[6], eq[6], rd[s].c, own);
+        cmp_step(lt[7], eq[7], from_east(rd[s].c, rd[s].r), own);
+    }
+    uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
+    ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
+    ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
 }
 
 // E planes from rank slices + the sweep-1 candidates (C, D = C, list).
@@ -441,27 +478,7 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
             if (pre) {
                 c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
                                           from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
-                uint32_t lt[8], eq[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    lt[k] = 0;
-                    eq[k] = ~0u;
-                }
-#pragma unroll
-                for (int s = S - 1; s >= 0; --s) {
-                    const uint32_t own = rm[s].c;
-                    cmp_step(lt[0], eq[0], from_west(ru[s].l, ru[s].c), own);
-                    cmp_step(lt[1], eq[1], ru[s].c, own);
-                    cmp_step(lt[2], eq[2], from_east(ru[s].c, ru[s].r), own);
-                    cmp_step(lt[3], eq[3], from_west(rm[s].l, rm[s].c), own);
-                    cmp_step(lt[4], eq[4], from_east(rm[s].c, rm[s].r), own);
-                    cmp_step(lt[5], eq[5], from_west(rd[s].l, rd[s].c), own);
-                    cmp_step(lt[6], eq[6], rd[s].c, own);
-                    cmp_step(lt[7], eq[7], from_east(rd[s].c, rd[s].r), own);
-                }
-                uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
-                ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
-                ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
+                store_e<S>(g, p, ru, rm, rd);
             }
             g.C[p] = c;
             g.D[p] = c;
@@ -476,6 +493,85 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
         }
     };
     walk_strips(g, [&](int x, int y0, int y1, int) { strip(x, y0, y1); });
+    add_count(cnt, counter);
+}
+
+// Fused prep + E-pass for images whose rows fit in a warp (WW divides 32 and
+// every thread walks one strip): each thread computes the rank slices of its
+// own word row by row and keeps a 3-row window; the slices of the left / right
+// words (the neighbouring lanes, same row, same step) come by warp shuffles,
+// so the slices never touch memory and the two phases need no barrier between.
+template <int FG, int R>
+__device__ __forceinline__ void prep_fused(const Img &g, bool thin, int xmode, bool save_xs, int t, int *counter) {
+    constexpr int S = Lev<R>::S;
+    const int lane = threadIdx.x & 31;
+    const int x = g.tid % g.WW, blk = g.tid / g.WW;
+    const bool act = blk < g.nblk;
+    const int y0 = act ? blk * g.hb : 0, y1 = act ? min(g.H, y0 + g.hb) : 0;
+    const bool hasl = x > 0, hasr = x < g.WW - 1;
+    int cnt = 0;
+    // rank slices of row y of this column (with the left / right words' by
+    // shuffle; all lanes take part in every step)
+    auto row = [&](int y, Row3 (&r)[S], uint32_t &bl) {
+        const bool in = act && y >= 0 && y < g.H;
+        uint32_t rs[S];
+        bl = ~0u;
+        if (in) {
+            const int p = pidx(g, y, x);
+            const uint32_t xs = g.I[p];
+            bl = rank_word<R>(g, y, x, p, thin, xmode, rs);
+            if (y >= y0 && y < y1) {
+                g.B[p] = bl;
+                if (save_xs) g.XS[p] = xs;
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < S; ++s) rs[s] = 0;
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const uint32_t l = __shfl_up_sync(0xffffffffu, rs[s], 1);
+            const uint32_t rr = __shfl_down_sync(0xffffffffu, rs[s], 1);
+            r[s] = Row3{hasl ? l : 0u, rs[s], hasr ? rr : 0u};
+        }
+    };
+    Row3 ru[S], rm[S], rd[S];
+    uint32_t bu, bm, bd;
+    row(y0 - 1, ru, bu);
+    row(y0, rm, bm);
+    const int steps = g.hb;   // warp-uniform trip count (shorter strips idle)
+    int p = pidx(g, y0, x);
+    Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
+    for (int j = 0; j < steps; ++j, p += g.S) {
+        const int y = y0 + j;
+        row(y + 1, rd, bd);
+        if (y < y1) {
+            const Row3 id = row3(g.I, p + g.S);
+            // E is read only for words holding candidates in some sweep of this
+            // engine call, and those lie inside the unblocked target pixels
+            const uint32_t pre = (t ? im.c : ~im.c) & ~bm;
+            uint32_t c = 0;
+            if (pre) {
+                c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
+                                          from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
+                store_e<S>(g, p, ru, rm, rd);
+            }
+            g.C[p] = c;
+            g.D[p] = c;
+            cnt += c != 0;
+            iu = im;
+            im = id;
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            ru[s] = rm[s];
+            rm[s] = rd[s];
+        }
+        bu = bm;
+        bm = bd;
+    }
+    (void)lane;
+    (void)bu;
     add_count(cnt, counter);
 }
 
@@ -1021,6 +1117,32 @@ __device__ __forceinline__ void epass_dispatch_v(const View &v, int S, int t, in
     }
 }
 static_assert(kMaxSlices <= 7, "epass_dispatch covers up to 7 rank slices");
+
+template <int FG, bool HOT, int R>
+__device__ __noinline__ void prep_fused_nl(const View v, bool thin, int xmode, bool save_xs, int t, int cur) {
+    const Img g = make_img<HOT>(v);
+    prep_fused<FG, R>(g, thin, xmode, save_xs, t, &g.sh->counters[cur]);
+}
+
+// fused prep + E-pass (see prep_fused); false when not eligible
+template <int FG, bool HOT>
+__device__ __forceinline__ bool prep_fused_dispatch_v(int r, const View &v, bool thin, int xmode, bool save_xs, int t,
+                                                      int cur) {
+    // must agree with the host planner (make_plan_fixed: no R planes then)
+    if (!HOT || v.nstrips > kThreads || (32 % v.WW) != 0) return false;
+    switch (r) {
+#define TS_FUSED_CASE(RR)                                            \
+    case RR:                                                          \
+        prep_fused_nl<FG, HOT, RR>(v, thin, xmode, save_xs, t, cur); \
+        return true;
+        TS_FUSED_CASE(1) TS_FUSED_CASE(2) TS_FUSED_CASE(3) TS_FUSED_CASE(4)
+        TS_FUSED_CASE(5) TS_FUSED_CASE(6) TS_FUSED_CASE(7) TS_FUSED_CASE(8)
+#undef TS_FUSED_CASE
+        default:
+            return false;
+    }
+}
+static_assert(kFusedMaxR == 8, "prep_fused_dispatch_v covers radii 1..8");
 
 template <int FG, bool HOT>
 __device__ __noinline__ void epass_prio_nl(const View v, const int64_t *prio, int t, int cur) {
@@ -1650,10 +1772,16 @@ __device__ __forceinline__ void run_stage(const View &v, const Img &gt, int r, b
                                           Shared &sh, int &cur, int *err, Stats &st, int &pc) {
     if (gt.tid == 0) sh.counters[cur] = 0;
     const long long tp0 = st.timing ? clock64() : 0;
-    const int S = prep_dispatch_v<HOT>(r, v, thin, xmode, save_xs);
-    team_sync(gt);
-    if (st.timing) st.cyc_rank += clock64() - tp0;
-    epass_dispatch_v<FG, HOT>(v, S, thin ? 1 : 0, cur);
+#ifndef TS_FUSED
+#define TS_FUSED 1
+#endif
+    if (!(TS_FUSED && prep_fused_dispatch_v<FG, HOT>(r, v, thin, xmode, save_xs, thin ? 1 : 0, cur))) {
+        // the counter reset above must land before the E-pass counts
+        const int S = prep_dispatch_v<HOT>(r, v, thin, xmode, save_xs);
+        team_sync(gt);
+        if (st.timing) st.cyc_rank += clock64() - tp0;
+        epass_dispatch_v<FG, HOT>(v, S, thin ? 1 : 0, cur);
+    }
     team_sync(gt);
     if (st.timing) st.cyc_prep += clock64() - tp0;
     engine<FG, HOT>(v, thin ? 1 : 0, -1, sh, cur, err, st, pc);

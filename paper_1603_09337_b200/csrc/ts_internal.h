@@ -13,6 +13,9 @@ namespace ts {
 // plane length `plen` words.
 constexpr int kPadRows = 1;
 
+// largest radius of the fused prep + E-pass (rank slices kept in registers)
+constexpr int kFusedMaxR = 8;
+
 // threads per CTA of the fused kernel (host planning must agree)
 #ifndef TS_THREADS
 #define TS_THREADS 512
