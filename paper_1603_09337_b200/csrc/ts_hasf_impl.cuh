@@ -1004,6 +1004,7 @@ struct Shared {
     long long dtime[4];  // stats: dense pass-1 / collect / list-pass cycles, listed words
     long long sstat[4];  // stats: list sweeps (33..512 words) count / cycles, (> 512) count / cycles
     long long bstat[4];  // stats, list sweeps > 512 words: list-build / sweep / re-examination cycles, list builds
+    long long xstat[4];  // stats: tiny regimes (incl. list build and barriers) cycles / count; 2-3 spare
 };
 
 // per-team control block in global memory (teams of G > 1 CTAs)
@@ -1662,6 +1663,10 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
             st.passes += *reinterpret_cast<volatile long long *>(&sh.tiny[1]);
             const bool tbad = *reinterpret_cast<volatile int *>(&sh.bad) != 0;
             __syncthreads();   // shared results read before they can be rewritten
+            if (st.timing && tid == 0) {
+                sh.xstat[0] += clock64() - tj0;
+                sh.xstat[1] += 1;
+            }
             if (tbad) {
                 if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
                 break;
@@ -1909,6 +1914,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.dtime[0] = sh.dtime[1] = sh.dtime[2] = sh.dtime[3] = 0;
             sh.sstat[0] = sh.sstat[1] = sh.sstat[2] = sh.sstat[3] = 0;
             sh.bstat[0] = sh.bstat[1] = sh.bstat[2] = sh.bstat[3] = 0;
+            sh.xstat[0] = sh.xstat[1] = sh.xstat[2] = sh.xstat[3] = 0;
         }
         load_image_nl<HOT>(v, &p, pix);
         team_sync(gk);
@@ -1959,6 +1965,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
                 sp[16 + k] = *reinterpret_cast<volatile long long *>(&sh.sstat[k]);
                 sp[20 + k] = *reinterpret_cast<volatile long long *>(&sh.dtime[k]);
                 sp[24 + k] = *reinterpret_cast<volatile long long *>(&sh.bstat[k]);
+                sp[28 + k] = *reinterpret_cast<volatile long long *>(&sh.xstat[k]);
             }
         }
         team_sync(gk);
