@@ -32,6 +32,9 @@ sys.path.insert(0, REPO)
 from paper_1603_09337_b200 import workloads as W  # noqa: E402
 
 METRIC = "HASF images/s (512^2 batch, 1 B200), % HBM roofline, vs CPU ref"
+E2E_PATH = {True: "ts_hasf_batch_host (C ABI, pinned host buffers; one fused launch fed by streamed H2D chunks, "
+                  "chunk-gated D2H)",
+            False: "ts_hasf_batch_host (C ABI, pinned host buffers; chunked H2D / kernel / D2H pipeline)"}
 PAPER_CPU_IMG_S = 32.0   # PAPER.md:13,330 (2x Xeon E5405, unknown r / images): context only
 
 
@@ -181,6 +184,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: = steps")
     ap.add_argument("--verify", type=int, default=2, help="images checked bit-exact vs the oracle")
+    ap.add_argument("--host-streaming", type=int, default=1,
+                    help="e2e host entry: 1 = one launch fed by streamed chunks, 0 = chunked launches")
     args = ap.parse_args()
     cfg = W.CONFIGS[args.config]
     if args.batch > 0:
@@ -262,6 +267,7 @@ def main():
 
     # e2e through the C ABI host-buffer entry, pinned host memory
     e2e_steps = args.e2e_steps or args.steps
+    lib.ts_set_host_streaming(args.host_streaming)
     hin = torch.from_numpy(imgs_np).pin_memory()
     hout = torch.empty_like(hin).pin_memory()
 
@@ -323,7 +329,7 @@ def main():
                          "kernel": "ts::hasf_kernel (one launch per step)"},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": cfg.n * cfg.h * cfg.w,
                     "d2h_bytes_per_step": cfg.n * cfg.h * cfg.w, "wall_ms": wall_ms,
-                    "path": "ts_hasf_batch_host (C ABI, pinned host buffers; chunked H2D / kernel / D2H pipeline)"},
+                    "path": E2E_PATH[args.host_streaming != 0]},
             "gpu_launches": args.steps,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

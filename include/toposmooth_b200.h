@@ -147,6 +147,13 @@ int32_t ts_set_team_size(int32_t ctas);
  * (0 = automatic: 256 x 2 when the hot planes fit half an SM).  Returns the previous value. */
 int32_t ts_set_cta_threads(int32_t threads);
 
+/* Tuning / A-B: 1 (default) = ts_hasf_batch_host runs ONE fused launch that
+ * starts while the input chunks are still being copied (stream memory
+ * operations gate each image on its chunk and each chunk's copy-back on its
+ * images); 0 = the chunked pipeline of separate launches.  Returns the
+ * previous value. */
+int32_t ts_set_host_streaming(int32_t on);
+
 /* Placement/occupancy the fused kernel would use for an image shape:
  * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
  * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA,

@@ -326,6 +326,8 @@ const char *err_message(int code, int mode) {
             return "internal: engine exceeded its sweep bound";
         case ERR_TEAM_TIMEOUT:
             return "internal: team barrier timed out";
+        case ERR_INPUT_TIMEOUT:
+            return "internal: streamed input chunk never arrived";
         default:
             return "internal: unknown device error";
     }
@@ -350,7 +352,8 @@ int check_fg(int32_t fg) {
 // non-null it receives the team size chosen.
 int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last,
                  int do_cut, int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, const int64_t *prio,
-                 long long max_sweeps, cudaStream_t st, int64_t *stats_host, int *err_dev, int *team_out) {
+                 long long max_sweeps, cudaStream_t st, int64_t *stats_host, int *err_dev, int *team_out,
+                 const unsigned *ready = nullptr, unsigned *done = nullptr, int chunk = 1) {
     int rc;
     if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
     if (r_last > kMaxR)
@@ -427,6 +430,9 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.team = team;
     p.threads = pl.threads;
     p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
+    p.ready = ready;
+    p.done = done;
+    p.chunk = chunk;
     cudaError_t le = launch_hasf(p, fg, grid, pl.smem_bytes, st);
     cudaError_t ce = cudaSuccess;
     if (le == cudaSuccess && stats_host)
@@ -439,7 +445,8 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
 }
 
 int device_error(int herr, int mode) {
-    const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP || herr == ERR_TEAM_TIMEOUT;
+    const bool internal = herr == ERR_JACOBI_CAP || herr == ERR_SWEEP_CAP || herr == ERR_TEAM_TIMEOUT ||
+                          herr == ERR_INPUT_TIMEOUT;
     return fail(internal ? TS_ERR_INTERNAL : TS_ERR_VALUE, err_message(herr, mode));
 }
 
@@ -511,6 +518,156 @@ int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
                      (cudaStream_t)stream, stats_host);
 }
 
+// ---- streamed host entry ---------------------------------------------------
+// One fused launch over the whole batch while the inputs are still arriving:
+// the copy-in stream copies chunk k and then writes ready[k] = 1 (a stream
+// memory operation, executed in stream order after the copy); CTAs wait for
+// their image's chunk flag; each finished image counts itself in done[k]; the
+// copy-out stream waits (stream memory operation) until done[k] reaches the
+// chunk's size and copies the chunk back.  The GPU therefore fills as soon as
+// the first chunk lands and no chunk boundary idles SMs.  The driver entry
+// points are resolved at run time (no link-time libcuda dependency).
+typedef int (*StreamWriteValue32Fn)(void *, unsigned long long, unsigned int, unsigned int);
+typedef int (*StreamWaitValue32Fn)(void *, unsigned long long, unsigned int, unsigned int);
+constexpr unsigned kWaitGeq = 0x0;        // CU_STREAM_WAIT_VALUE_GEQ
+constexpr unsigned kWriteDefault = 0x0;   // CU_STREAM_WRITE_VALUE_DEFAULT (fence before the write)
+
+struct MemOps {
+    StreamWriteValue32Fn write = nullptr;
+    StreamWaitValue32Fn wait = nullptr;
+};
+const MemOps &memops() {
+    static const MemOps m = [] {
+        MemOps r;
+        void *fw = nullptr, *fv = nullptr;
+        cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = cudaDriverEntryPointSymbolNotFound;
+        // the CUDA 12 (v2) memory operations, which need no device opt-in
+        if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &fw, 12000, cudaEnableDefault, &q1) ==
+                cudaSuccess &&
+            cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &fv, 12000, cudaEnableDefault, &q2) ==
+                cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+            r.write = (StreamWriteValue32Fn)fw;
+            r.wait = (StreamWaitValue32Fn)fv;
+        }
+        return r;
+    }();
+    return m;
+}
+std::atomic<int> g_streamed{1};
+
+// chunk flag buffers for the streamed entry: plain cudaMalloc allocations
+// (stream memory operations target them), recycled, never freed
+constexpr int kMaxChunks = 64;
+std::mutex g_flag_mu;
+std::vector<std::pair<int, unsigned *>> g_flag_free;   // (device, buffer of 2 * kMaxChunks)
+
+unsigned *take_flags(int dev) {
+    {
+        std::lock_guard<std::mutex> lk(g_flag_mu);
+        for (size_t i = 0; i < g_flag_free.size(); ++i)
+            if (g_flag_free[i].first == dev) {
+                unsigned *b = g_flag_free[i].second;
+                g_flag_free.erase(g_flag_free.begin() + (long)i);
+                return b;
+            }
+    }
+    unsigned *b = nullptr;
+    if (cudaMalloc((void **)&b, 2 * kMaxChunks * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    return b;
+}
+void give_flags(int dev, unsigned *b) {
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    g_flag_free.emplace_back(dev, b);
+}
+
+int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                       int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host, cudaStream_t user,
+                       const MemOps &mo) {
+    const size_t img = (size_t)h * w, bytes = (size_t)n * img;
+    // chunks of ~4 MB (16 images at 512^2), at most 64 of them
+    int64_t chunk = std::max<int64_t>(1, (int64_t)((4u << 20) / std::max<size_t>(img, 1)));
+    chunk = std::max<int64_t>(chunk, (n + kMaxChunks - 1) / kMaxChunks);
+    const int nchunks = (int)((n + chunk - 1) / chunk);
+    const int nbuf = 2 + (keep_host ? 1 : 0) + (avoid_host ? 1 : 0);
+    uint8_t *d = nullptr;
+    int *err = nullptr;
+    unsigned *flags = nullptr;   // ready[nchunks], done[nchunks]
+    TS_CUDA(cudaMallocAsync((void **)&d, bytes * nbuf, user));
+    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
+    int dev = 0;
+    TS_CUDA(cudaGetDevice(&dev));
+    flags = take_flags(dev);
+    if (!flags) return fail(TS_ERR_CUDA, "cudaMalloc(chunk flags)");
+    TS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), user));
+    TS_CUDA(cudaMemsetAsync(flags, 0, 2 * nchunks * sizeof(unsigned), user));
+    uint8_t *din = d, *dout = d + bytes;
+    uint8_t *dk = keep_host ? d + 2 * bytes : nullptr;
+    uint8_t *da = avoid_host ? d + (2 + (keep_host ? 1 : 0)) * bytes : nullptr;
+    unsigned *ready = flags, *done = flags + nchunks;
+    cudaStream_t sin = nullptr, sout = nullptr, sc = nullptr;
+    cudaEvent_t ev0 = nullptr, ec = nullptr, eo = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ec, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eo, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev0, user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, ev0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev0, 0);
+    int rc = TS_OK, mrc = 0;
+    for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
+        const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+        const size_t off = (size_t)i0 * img, sz = (size_t)cnt * img;
+        e = cudaMemcpyAsync(din + off, in_host + off, sz, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess && dk) e = cudaMemcpyAsync(dk + off, keep_host + off, sz, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess && da) e = cudaMemcpyAsync(da + off, avoid_host + off, sz, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) mrc = mo.write(sin, (unsigned long long)(uintptr_t)(ready + k), 1u, kWriteDefault);
+    }
+    if (e == cudaSuccess && mrc == 0)
+        rc = fused_launch(MODE_HASF, din, dout, n, h, w, 1, r_max, 1, 1, fg, dk, da, nullptr, -1, sc, nullptr, err,
+                          nullptr, ready, done, (int)chunk);
+    if (e == cudaSuccess && mrc == 0 && rc == TS_OK) {
+        for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
+            const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+            const size_t off = (size_t)i0 * img, sz = (size_t)cnt * img;
+            mrc = mo.wait(sout, (unsigned long long)(uintptr_t)(done + k), (unsigned)cnt, kWaitGeq);
+            if (mrc == 0) e = cudaMemcpyAsync(out_host + off, dout + off, sz, cudaMemcpyDeviceToHost, sout);
+        }
+    }
+    cudaEventRecord(ec, sc);
+    cudaEventRecord(eo, sout);
+    cudaStreamWaitEvent(user, ec, 0);
+    cudaStreamWaitEvent(user, eo, 0);
+    int herr = 0;
+    cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, user);
+    const std::string keep_msg = g_err;
+    cudaFreeAsync(d, user);
+    cudaFreeAsync(err, user);
+    cudaError_t se = cudaStreamSynchronize(user);
+    give_flags(dev, flags);   // idle again once the stream drained
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ec);
+    cudaEventDestroy(eo);
+    cudaStreamDestroy(sin);
+    cudaStreamDestroy(sout);
+    cudaStreamDestroy(sc);
+    if (rc) {
+        g_err = keep_msg;
+        return rc;
+    }
+    if (mrc) return fail(TS_ERR_CUDA, "stream memory operation failed (code " + std::to_string(mrc) + ")");
+    if (e != cudaSuccess) return cuda_fail(e, "streamed host path");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
+    if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
+    if (herr) return device_error(herr, MODE_HASF);
+    return ok();
+}
+
+int32_t ts_set_host_streaming(int32_t on) { return g_streamed.exchange(on ? 1 : 0); }
+
 int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w, int32_t r_max,
                        int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host, void *stream) {
     // Pipelined: the batch is cut into chunks; chunk k's H2D copy (copy-in
@@ -525,6 +682,9 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     cudaStream_t user = (cudaStream_t)stream;
     const size_t img = (size_t)h * w, bytes = (size_t)n * img;
     const bool big = (long long)h * w > 1024LL * 1024;   // team-sized images: one chunk
+    const MemOps &mo = memops();
+    if (!big && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR)
+        return hasf_host_streamed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);
     const int nchunks = big ? 1 : (int)std::min<int64_t>(n, 4);
     const int ncs = 3;   // compute streams
     const int64_t per = (n + nchunks - 1) / nchunks;

@@ -1906,6 +1906,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         team_sync(gk);
         const int img = *reinterpret_cast<volatile int *>(&sh.img);
         if (img >= p.n) break;
+        if (p.ready) {   // streamed host entry: wait for the image's input chunk
+            if (lead) {
+                const unsigned *f = p.ready + img / p.chunk;
+                long long spins = 0;
+                unsigned v;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    if (v) break;
+                    __nanosleep(256);
+                    if (++spins > (1LL << 24)) {   // seconds: the copy never came
+                        set_err(p.err, ERR_INPUT_TIMEOUT);
+                        break;
+                    }
+                }
+            }
+            team_sync(gk);
+        }
         const size_t pix = (size_t)img * p.H * p.W;
         if (lead) {
             sh.counters[0] = 0;
@@ -1969,6 +1986,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             }
         }
         team_sync(gk);
+        if (p.done && lead) {   // all the image's output stored: publish it to the copy-out stream
+            __threadfence_system();
+            atomicAdd(p.done + img / p.chunk, 1u);
+        }
     }
 }
 

@@ -70,6 +70,7 @@ enum Err : int {
     ERR_CONSTRAINT_NOT_BINARY = 7,
     ERR_ALLOWED_NOT_SUPERSET = 8,  // thicken: object outside allowed
     ERR_TEAM_TIMEOUT = 9,      // a team barrier did not complete (CTA not co-resident)
+    ERR_INPUT_TIMEOUT = 10,    // streamed host entry: an input chunk never arrived
 };
 
 struct KParams {
@@ -97,6 +98,12 @@ struct KParams {
     int hot;                // I, D, C, B, DIRTY, MARK all in shared memory (fast variant)
     long long off[B_COUNT]; // word offset of each buffer (smem or CTA slice)
     int *counter;           // image queue head
+    // streamed host entry (or null): image i waits for ready[i / chunk] != 0
+    // (written by the copy-in stream after the chunk's H2D copy) and, once
+    // stored, counts itself in done[i / chunk] (awaited by the copy-out stream)
+    const unsigned *ready;
+    unsigned *done;
+    int chunk;
     int *err;               // first error code (atomicCAS from 0)
     long long *stats;       // [n][kStatFields] (or null), see kStatFields
 };
