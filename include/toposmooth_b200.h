@@ -134,7 +134,7 @@ int ts_selftest_circuit(uint8_t *s84_256_host, uint8_t *s48_256_host);
 int64_t ts_set_smem_budget(int64_t bytes);
 
 /* Tuning: a sweep runs in dense (strip-walk) mode when more than
- * (words / div) words hold candidates (default and minimum div = 2).  Returns the
+ * (words / div) words hold candidates (default 4, minimum 2).  Returns the
  * previous value. */
 int32_t ts_set_dense_divisor(int32_t div);
 

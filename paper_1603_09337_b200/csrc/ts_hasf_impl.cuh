@@ -665,7 +665,7 @@ __device__ __forceinline__ uint32_t decide(uint32_t c, const Nb &i, const Nb &d,
 // checks and E loads (from L2 when E does not fit in shared memory) are issued
 // together, then the rows are evaluated in order with the sliding window.
 #ifndef TS_DENSE_BATCH
-#define TS_DENSE_BATCH 4
+#define TS_DENSE_BATCH 2
 #endif
 constexpr int kDenseBatch = TS_DENSE_BATCH;
 
