@@ -154,6 +154,12 @@ int32_t ts_set_cta_threads(int32_t threads);
  * previous value. */
 int32_t ts_set_host_streaming(int32_t on);
 
+/* Tuning / A-B: 1 (default) = where eligible (one strip per thread, rows of
+ * <= 32 words tiling a warp, r <= 8) the rank slices of the clamped EDT stay in
+ * registers (fused prep + E-pass); 0 = always the two-phase prep / E-pass
+ * through the rank planes.  Returns the previous value. */
+int32_t ts_set_fused_prep(int32_t on);
+
 /* Placement/occupancy the fused kernel would use for an image shape:
  * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
  * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA,

@@ -48,6 +48,7 @@ SIGNATURES = {
     "ts_set_team_size": ([_i32], _i32),
     "ts_set_cta_threads": ([_i32], _i32),
     "ts_set_host_streaming": ([_i32], _i32),
+    "ts_set_fused_prep": ([_i32], _i32),
     "ts_hasf_plan": ([_i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int),
 }
 

@@ -114,6 +114,7 @@ struct Plan {
     int WW = 0, nwords = 0, slices = 0;
     int stride = 0, plen = 0, nblk = 1, hb = 1, nstrips = 1, dense_min = 0;
     int pad = kPadRows;
+    bool fused = false;   // fused prep + E-pass (no R planes)
     int per_sm = 0, per_wave = 0;
     size_t smem_bytes = 0;
     uint32_t mask = 0;
@@ -123,6 +124,7 @@ struct Plan {
     long long stride_ws = 0;   // global workspace words per CTA
 };
 
+std::atomic<int> g_fused{1};      // fused prep + E-pass where eligible
 std::atomic<int> g_dense_div{4};   // measured: 4 beats 2 by ~1.5% on c1, neutral on c4
 
 // strip mapping (thread t -> word column t % WW, row block t / WW) and the
@@ -222,6 +224,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     pl.plen = (int)plen;
     pl.nwords = H * pl.WW;
     pl.dense_min = pl.nwords / std::max(1, g_dense_div.load());
+    pl.fused = false;
     pl.slices = (mode == MODE_HASF && r_last >= 1) ? rank_slices(r_last) : 0;
     auto r4 = [](long long x) { return (x + 3) & ~3LL; };
     long long size[B_COUNT];
@@ -237,8 +240,9 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     // the fused prep + E-pass (one strip per thread, rows of <= 32 words that
     // tile a warp, r <= 8) keeps the rank slices in registers: no R planes
     const bool fused = mode == MODE_HASF && team == 1 && pl.nstrips <= threads && 32 % pl.WW == 0 &&
-                       r_last <= kFusedMaxR && !skip_fused;
+                       r_last <= kFusedMaxR && !skip_fused && g_fused.load();
     size[B_R] = fused ? 0 : (long long)pl.slices * plen;
+    pl.fused = fused;
     size[B_K] = (mode == MODE_HASF && has_k) ? plen : 0;
     size[B_A] = (mode == MODE_HASF && has_a) ? plen : 0;
 
@@ -430,6 +434,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.team = team;
     p.threads = pl.threads;
     p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
+    p.fused = pl.fused ? 1 : 0;
     p.ready = ready;
     p.done = done;
     p.chunk = chunk;
@@ -667,6 +672,8 @@ int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
 }
 
 int32_t ts_set_host_streaming(int32_t on) { return g_streamed.exchange(on ? 1 : 0); }
+
+int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
 
 int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w, int32_t r_max,
                        int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host, void *stream) {

@@ -1023,7 +1023,7 @@ static_assert(sizeof(TeamCtl) <= kTeamCtlBytes, "kTeamCtlBytes too small");
 struct View {
     unsigned long long I, D, C, dirty, mark;   // shared address (HOT) or pointer bits
     uint32_t *B, *list, *E, *XS, *R, *K, *A;
-    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min;
+    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, fused;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank;
@@ -1129,8 +1129,8 @@ __device__ __noinline__ void prep_fused_nl(const View v, bool thin, int xmode, b
 template <int FG, bool HOT>
 __device__ __forceinline__ bool prep_fused_dispatch_v(int r, const View &v, bool thin, int xmode, bool save_xs, int t,
                                                       int cur) {
-    // must agree with the host planner (make_plan_fixed: no R planes then)
-    if (!HOT || v.nstrips > kThreads || (32 % v.WW) != 0) return false;
+    // the host planner decided (make_plan_fixed: no R planes then)
+    if (!HOT || !v.fused) return false;
     switch (r) {
 #define TS_FUSED_CASE(RR)                                            \
     case RR:                                                          \
@@ -1888,6 +1888,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     v.nblk = p.nblk;
     v.hb = p.hb;
     v.nstrips = p.nstrips;
+    v.fused = p.fused;
     v.dense_min = p.dense_min;
     v.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
     v.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;

@@ -104,6 +104,7 @@ struct KParams {
     const unsigned *ready;
     unsigned *done;
     int chunk;
+    int fused;              // 1: fused prep + E-pass allowed (the planner left out the R planes)
     int *err;               // first error code (atomicCAS from 0)
     long long *stats;       // [n][kStatFields] (or null), see kStatFields
 };

@@ -302,3 +302,65 @@ def test_topology_counts_full_size_outputs():
     fi, bi = P.topology_counts(img[None])
     fo, bo = P.topology_counts(out[None])
     assert fi[0] == fo[0] == O.component_count(img, 8) and bi[0] == bo[0] == O.background_component_count(img, 4)
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+def test_fused_and_two_phase_prep_vs_oracle(fused):
+    """The fused prep + E-pass (rank slices in registers, neighbours by warp
+    shuffle) and the two-phase prep / E-pass through rank planes give the
+    oracle's output; shapes chosen on both sides of the fused path's
+    eligibility (rows of 1, 2, 4, 8, 16 words; r up to 8; a 3-word row)."""
+    lib = _lib.load()
+    old = lib.ts_set_fused_prep(fused)
+    try:
+        rng = np.random.default_rng(500 + fused)
+        for (h, w, fg, r) in [(96, 32, 8, 2), (64, 64, 4, 3), (80, 128, 8, 8), (40, 256, 8, 5), (50, 512, 4, 4),
+                              (70, 90, 8, 6)]:
+            imgs = np.stack([random_image(rng, h, w, rng.uniform(0.3, 0.7)) for _ in range(3)])
+            adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+            assert np.array_equal(P.hasf_batch(imgs, r, adj), O.hasf_batch(imgs, r, fg, threads=4)), (fused, h, w, r)
+        imgs = W.config_batch("c1", 1100, 2)
+        assert np.array_equal(P.hasf_batch(imgs, 5), O.hasf_batch(imgs, 5, 8, threads=2))
+        keep = (imgs & (rng.random(imgs.shape) < 0.02)).astype(np.uint8)
+        avoid = ((rng.random(imgs.shape) < 0.02) & (imgs == 0)).astype(np.uint8)
+        assert np.array_equal(P.hasf_batch(imgs, 3, P.ADJ_84, keep=keep, avoid=avoid),
+                              O.hasf_batch(imgs, 3, 8, keep=keep, avoid=avoid, threads=2))
+    finally:
+        lib.ts_set_fused_prep(old)
+
+
+@pytest.mark.parametrize("streaming", [1, 0])
+def test_streamed_host_entry_vs_device_path(streaming):
+    """ts_hasf_batch_host: one launch gated on streamed input chunks (and
+    chunk-gated copy-back), or the chunked pipeline -- against the
+    device-resident path, for batch sizes around the chunk size (16 images of
+    512^2), a single image, other shapes and keep / avoid constraints."""
+    lib = _lib.load()
+    old = lib.ts_set_host_streaming(streaming)
+    try:
+        stream = torch.cuda.current_stream().cuda_stream
+        for cfg, start, n in (("c1", 1200, 1), ("c1", 1210, 17), ("c1", 1230, 40), ("c4", 4100, 70)):
+            c = W.CONFIGS[cfg]
+            imgs = W.config_batch(c, start, n)
+            adj = P.ADJ_84 if c.fg == 8 else P.ADJ_48
+            want = P.hasf_batch(imgs, c.r_max, adj)
+            hin = torch.from_numpy(imgs).pin_memory()
+            hout = torch.zeros_like(hin).pin_memory()
+            _lib.check(lib.ts_hasf_batch_host(hin.data_ptr(), hout.data_ptr(), n, c.h, c.w, c.r_max, c.fg, None, None,
+                                              stream))
+            assert np.array_equal(hout.numpy(), want), (streaming, cfg, n)
+        assert np.array_equal(want[:2], O.hasf_batch(imgs[:2], 4, 4, threads=2))
+        rng = np.random.default_rng(77)
+        imgs = np.stack([random_image(rng, 100, 96, 0.5) for _ in range(5)])
+        keep = (imgs & (rng.random(imgs.shape) < 0.05)).astype(np.uint8)
+        avoid = ((rng.random(imgs.shape) < 0.05) & (imgs == 0)).astype(np.uint8)
+        out = np.zeros_like(imgs)
+        _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, 5, 100, 96, 3, 8, keep.ctypes.data,
+                                          avoid.ctypes.data, stream))
+        assert np.array_equal(out, O.hasf_batch(imgs, 3, 8, keep=keep, avoid=avoid, threads=4))
+        bad = imgs.copy()
+        bad[2, 5, 5] = 7
+        rc = lib.ts_hasf_batch_host(bad.ctypes.data, out.ctypes.data, 5, 100, 96, 3, 8, None, None, stream)
+        assert rc == _lib.TS_ERR_VALUE and b"0 or 1" in lib.ts_last_error()
+    finally:
+        lib.ts_set_host_streaming(old)
