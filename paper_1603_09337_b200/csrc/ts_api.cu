@@ -114,6 +114,7 @@ struct Plan {
     int WW = 0, nwords = 0, slices = 0;
     int stride = 0, plen = 0, nblk = 1, hb = 1, nstrips = 1, dense_min = 0;
     int pad = kPadRows;
+    int mwords = 0;
     bool fused = false;   // fused prep + E-pass (no R planes)
     int per_sm = 0, per_wave = 0;
     size_t smem_bytes = 0;
@@ -233,6 +234,8 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     size[B_C] = plen;
     size[B_B] = plen;
     size[B_DIRTY] = r4((plen + 31) / 32);
+    size[B_CLAIM] = 2 * size[B_DIRTY];
+    pl.mwords = (int)size[B_DIRTY];
     size[B_MARK] = r4(((plen + 15) / 16) * 4);
     size[B_LIST] = 2 * plen;   // two compacted re-evaluation lists in dense sweeps
     size[B_E] = 8 * plen;
@@ -424,6 +427,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.hb = pl.hb;
     p.nstrips = pl.nstrips;
     p.pad = pl.pad;
+    p.mwords = pl.mwords;
     p.dense_min = pl.dense_min;
     p.smem_mask = pl.mask;
     p.hot = pl.hot ? 1 : 0;

@@ -70,6 +70,8 @@ struct Img {
     uint32_t *I, *D, *C, *dirty;          // hot planes
     uint8_t *mark;                        // hot: worklist pass stamps, one byte per word
     uint32_t *B, *list, *E, *XS, *R, *K, *A;  // smem or global (generic pointers)
+    uint32_t *claim;                      // 2 claim bitmaps of the compacted passes, mw words each
+    int mw;
     int H, W, WW;
     int S;          // padded row stride (words)
     int plen;       // padded plane length (words)
@@ -999,7 +1001,7 @@ struct Shared {
     int bad;
     unsigned long long flips, evals;
     long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
-    int lcount[2];       // lengths of the two compacted re-evaluation lists (dense sweeps)
+    int lcount[3];       // lengths of the compacted re-evaluation lists (rotating, see claim_passes)
     int dcount;          // dirty words listed for re-examination after a list sweep
     long long dtime[4];  // stats: dense pass-1 / collect / list-pass cycles, listed words
     long long sstat[4];  // stats: list sweeps (33..512 words) count / cycles, (> 512) count / cycles
@@ -1022,8 +1024,8 @@ static_assert(sizeof(TeamCtl) <= kTeamCtlBytes, "kTeamCtlBytes too small");
 // cvta inside the callee (so accesses compile to LDS/STS), others as pointers.
 struct View {
     unsigned long long I, D, C, dirty, mark;   // shared address (HOT) or pointer bits
-    uint32_t *B, *list, *E, *XS, *R, *K, *A;
-    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, fused;
+    uint32_t *B, *list, *E, *XS, *R, *K, *A, *claim;
+    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, fused, mw;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank;
@@ -1048,6 +1050,8 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.dirty = hot_ptr<HOT>(v.dirty);
     g.mark = reinterpret_cast<uint8_t *>(hot_ptr<HOT>(v.mark));
     g.B = v.B;
+    g.claim = v.claim;
+    g.mw = v.mw;
     g.list = v.list;
     g.E = v.E;
     g.XS = v.XS;
@@ -1372,85 +1376,93 @@ __device__ __forceinline__ bool commit_eval(const Img &g, const WordEval &w, uin
     return true;
 }
 
-// re-evaluate the listed words (two per thread at a time, so the loads of both
-// are in flight together); changes stamp the affected neighbour words `next`
-template <int FG>
-__device__ __forceinline__ bool list_pass(const Img &g, const uint32_t *list, int n, uint8_t next, int &evals) {
-    bool ch = false;
-    const int nthr = g.nthr;
-#ifndef TS_LIST2
-#define TS_LIST2 0
-#endif
-    if (!TS_LIST2) {
-        for (int sl = g.tid; sl < n; sl += nthr) {
-            WordEval a;
-            load_eval(g, (int)list[sl], a);
-            ch |= commit_eval(g, a, solve_eval<FG>(a), next);
-            ++evals;
-        }
-        return ch;
+// Compacted passes with claims: when a word's decisions change, each affected
+// neighbour word (E-directed, as in stamp_chg) that holds candidates is
+// claimed in the pass's claim bitmap; its first claimant appends it to the next
+// pass's list.  A pass that claims nothing ends the sweep (every candidate's
+// inputs are unchanged since its last evaluation).
+__device__ __forceinline__ void claim_chg(const Img &g, int p, uint32_t chg, uint4 e0, uint4 e1, uint32_t *Q,
+                                          uint32_t *next, int *ncount) {
+    const int S = g.S;
+    auto claim = [&](int q) {
+        if (g.C[q] == 0u) return;
+        const uint32_t bit = 1u << (q & 31);
+        if (atomicOr(&Q[q >> 5], bit) & bit) return;
+        next[atomicAdd(ncount, 1)] = (uint32_t)q;
+    };
+    const uint32_t lNW = ~e0.x, lN = ~e0.y, lNE = ~e0.z, lW = ~e0.w;   // "that neighbour is later"
+    const uint32_t lE = ~e1.x, lSW = ~e1.y, lS = ~e1.z, lSE = ~e1.w;
+    if (chg & (lN | (lNW & ~1u) | (lNE & 0x7FFFFFFFu))) claim(p - S);
+    if (chg & (lS | (lSW & ~1u) | (lSE & 0x7FFFFFFFu))) claim(p + S);
+    if (chg & 1u) {
+        if (lNW & 1u) claim(p - S - 1);
+        if (lW & 1u) claim(p - 1);
+        if (lSW & 1u) claim(p + S - 1);
     }
-    for (int sl = g.tid; sl < n; sl += 2 * nthr) {
-        const bool two = sl + nthr < n;
-        WordEval a, b;
+    if (chg >> 31) {
+        if (lNE >> 31) claim(p - S + 1);
+        if (lE >> 31) claim(p + 1);
+        if (lSE >> 31) claim(p + S + 1);
+    }
+}
+
+// pass j of a sweep's compacted phase: evaluate list (n words, in-word chains
+// resolved at once), claims into bitmap Q -> next; Qclear (the next pass's
+// bitmap, idle now) is cleared on the way
+template <int FG>
+__device__ __forceinline__ void claim_pass(const Img &g, const uint32_t *list, int n, uint32_t *Q, uint32_t *Qclear,
+                                           uint32_t *next, int *ncount, int &evals) {
+    for (int q = g.tid; q < g.mw; q += g.nthr) Qclear[q] = 0u;
+    for (int sl = g.tid; sl < n; sl += g.nthr) {
+        WordEval a;
         load_eval(g, (int)list[sl], a);
-        if (two) load_eval(g, (int)list[sl + nthr], b);
-        const uint32_t na = solve_eval<FG>(a);
-        const uint32_t nb = two ? solve_eval<FG>(b) : 0u;
-        ch |= commit_eval(g, a, na, next);
-        if (two) ch |= commit_eval(g, b, nb, next);
-        evals += two ? 2 : 1;
-    }
-    return ch;
-}
-
-// sweep-list words stamped `v` -> list (the sweep's candidates are all listed)
-__device__ __forceinline__ void filter_stamped(const Img &g, const uint32_t *from, int n, uint8_t v, uint32_t *list,
-                                               int *counter) {
-    const int lane = threadIdx.x & 31;
-    for (int s0 = g.tid - lane; s0 < n; s0 += g.nthr) {   // warp-uniform trip count
-        const int sl = s0 + lane;
-        const uint32_t p = sl < n ? from[sl] : 0u;
-        const bool has = sl < n && g.mark[p] == v;
-        const unsigned m = __ballot_sync(0xffffffffu, has);
-        if (m == 0) continue;
-        int base = 0;
-        if (lane == 0) base = atomicAdd(counter, __popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (has) list[base + __popc(m & ((1u << lane) - 1u))] = p;
+        const uint32_t nd = solve_eval<FG>(a);
+        ++evals;
+        if (nd != a.old) {
+            g.D[a.p] = nd;
+            claim_chg(g, a.p, nd ^ a.old, a.e0, a.e1, Q, next, ncount);
+        }
     }
 }
 
-// list sweep (> 32 listed words): one pass over the sweep list, then
-// compacted passes over the stamped words until none is stamped; then apply
+// Passes j, j+1, ... until one claims nothing.  Pass j reads lists[j & 1]
+// (n words), claims into bitmap j & 1 and list (j + 1) & 1 counted in
+// lcount[(j + 1) % 3], clears bitmap (j + 1) & 1 and zeroes lcount[(j + 2) % 3]
+// (last read before the previous barrier).  Between sweeps both bitmaps are
+// zero and lcount[] is reset by the engine after the post-sweep barrier.
 template <int FG>
-__device__ __forceinline__ SweepOut list_sweep(const Img &g, int n, long long cap, int pc0) {
-    SweepOut o{0, 0, 0, false};
-    int pc = pc0;
+__device__ __forceinline__ void claim_passes(const Img &g, uint32_t *const (&lists)[2], int j, int n, long long cap,
+                                             SweepOut &o) {
     Shared &sh = *g.sh;
-    uint32_t *lists[2] = {g.list + g.plen, g.list + g.plen + g.plen / 2};   // each >= nwords / 2 >= n
-    if (g.tid == 0) {
-        sh.lcount[1] = 0;
-        sh.dcount = 0;
-    }
-    list_pass<FG>(g, g.list, n, (uint8_t)(pc + 1), o.evals);
-    ++o.passes;
-    ++pc;
-    for (int k = 1;; k ^= 1) {
-        team_sync(g);
-        filter_stamped(g, g.list, n, (uint8_t)pc, lists[k], &sh.lcount[k]);
-        if (g.tid == 0) sh.lcount[k ^ 1] = 0;
-        team_sync(g);
-        const int m = *reinterpret_cast<volatile int *>(&sh.lcount[k]);
-        if (m == 0) break;
+    while (n > 0) {
         if (o.passes > cap) {
             o.bad = true;
             break;
         }
-        list_pass<FG>(g, lists[k], m, (uint8_t)(pc + 1), o.evals);
+        if (g.tid == 0) sh.lcount[(j + 2) % 3] = 0;
+        claim_pass<FG>(g, lists[j & 1], n, g.claim + (j & 1) * g.mw, g.claim + ((j + 1) & 1) * g.mw,
+                       lists[(j + 1) & 1], &sh.lcount[(j + 1) % 3], o.evals);
         ++o.passes;
-        ++pc;
+        team_sync(g);
+        n = *reinterpret_cast<volatile int *>(&sh.lcount[(j + 1) % 3]);
+        ++j;
     }
+}
+
+// list sweep (> 32 listed words): a claim pass over the sweep list, then
+// claim passes until none claims; then apply
+template <int FG>
+__device__ __forceinline__ SweepOut list_sweep(const Img &g, int n, long long cap, int pc0) {
+    SweepOut o{0, 0, 0, false};
+    (void)pc0;
+    Shared &sh = *g.sh;
+    uint32_t *const lists[2] = {g.list + g.plen, g.list + g.plen + g.plen / 2};   // each >= nwords / 2 >= n
+    if (g.tid == 0) sh.dcount = 0;
+    // pass 1 (j = 1): the sweep list; its claims become lists[0] (lcount[2])
+    claim_pass<FG>(g, g.list, n, g.claim + g.mw, g.claim, lists[0], &sh.lcount[2], o.evals);
+    ++o.passes;
+    team_sync(g);
+    claim_passes<FG>(g, lists, 2, *reinterpret_cast<volatile int *>(&sh.lcount[2]), cap, o);
     for (int sl = g.tid; sl < n; sl += g.nthr) {
         const int p = (int)g.list[sl];
         o.flips += apply_word(g, p, g.D[p]);
@@ -1465,42 +1477,34 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
     Shared &sh = *g.sh;
-    uint32_t *lists[2] = {g.list, g.list + g.plen};
+    uint32_t *const lists[2] = {g.list, g.list + g.plen};
     const bool tm = timing && g.tid == 0;
     long long t0 = tm ? clock64() : 0;
-    if (g.tid == 0) sh.lcount[1] = 0;
     if (HOT)
         dense_pass<FG>(g, pc, o.evals);
     else
         dense_pass_l2<FG>(g, true, pc, o.evals);
     ++o.passes;
     ++pc;
-    for (int k = 1;; k ^= 1) {
-        team_sync(g);   // stamps of the previous pass complete
-        if (tm) {
-            const long long t1 = clock64();
-            sh.dtime[o.passes == 1 ? 0 : 2] += t1 - t0;
-            t0 = t1;
-        }
-        collect_stamped(g, (uint8_t)pc, lists[k], &sh.lcount[k]);
-        if (g.tid == 0) sh.lcount[k ^ 1] = 0;   // the list after next (its last reader finished before the sync)
-        team_sync(g);
-        const int n = *reinterpret_cast<volatile int *>(&sh.lcount[k]);
-        if (tm) {
-            const long long t1 = clock64();
-            sh.dtime[1] += t1 - t0;
-            sh.dtime[3] += n;
-            t0 = t1;
-        }
-        if (n == 0) break;
-        if (o.passes > cap) {
-            o.bad = true;
-            break;
-        }
-        list_pass<FG>(g, lists[k], n, (uint8_t)(pc + 1), o.evals);
-        ++o.passes;
-        ++pc;
+    team_sync(g);   // stamps of the strip-walk pass complete
+    if (tm) {
+        const long long t1 = clock64();
+        sh.dtime[0] += t1 - t0;
+        t0 = t1;
     }
+    // the strip walk stamped densely: gather the stamped candidate words by a
+    // scan (j = 2's list, lcount[2]); later passes build their lists by claims
+    collect_stamped(g, (uint8_t)pc, lists[0], &sh.lcount[2]);
+    team_sync(g);
+    const int n2 = *reinterpret_cast<volatile int *>(&sh.lcount[2]);
+    if (tm) {
+        const long long t1 = clock64();
+        sh.dtime[1] += t1 - t0;
+        sh.dtime[3] += n2;
+        t0 = t1;
+    }
+    claim_passes<FG>(g, lists, 2, n2, cap, o);
+    if (tm) sh.dtime[2] += clock64() - t0;
     for_strip(g, [&](int y, int x, int p) {
         const uint32_t dw = g.D[p];
         if (dw) {
@@ -1683,6 +1687,7 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
             sh.counters[cur ^ 1] = 0;
         }
         team_sync(g);
+        if (tid == 0) sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = 0;   // all read before that barrier
         if (*reinterpret_cast<volatile int *>(&sh.bad)) {
             if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
             break;
@@ -1806,6 +1811,7 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
         g.B[q] = ~0u;   // pads blocked
     }
     for (int q = tid; q < (g.plen + 31) >> 5; q += nthr) g.dirty[q] = 0;
+    for (int q = tid; q < 2 * g.mw; q += nthr) g.claim[q] = 0;
     for (int q = tid; q < (g.plen + 15) >> 4; q += nthr)
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
     if (g.G > 1 && tid == 0) {
@@ -1873,6 +1879,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         v.mark = (unsigned long long)buf(B_MARK);
     }
     v.B = buf(B_B);
+    v.claim = buf(B_CLAIM);
+    v.mw = p.mwords;
     v.list = buf(B_LIST);
     v.E = buf(B_E);
     v.XS = buf(B_XS);
@@ -1927,6 +1935,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         const size_t pix = (size_t)img * p.H * p.W;
         if (lead) {
             sh.counters[0] = 0;
+            sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = 0;
             sh.flips = 0;
             sh.evals = 0;
             sh.dtime[0] = sh.dtime[1] = sh.dtime[2] = sh.dtime[3] = 0;

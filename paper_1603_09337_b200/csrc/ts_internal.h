@@ -38,12 +38,13 @@ enum Buf : int {
     B_R,         // rank bit-slices of the clamped distance map        S * plen
     B_K,         // keep constraint plane (optional)                   plen
     B_A,         // avoid constraint plane (optional)                  plen
+    B_CLAIM,     // 2 claim bitmaps of the compacted passes             2 * plen / 32
     B_COUNT
 };
 
 // shared-memory placement priority: the planes every fixpoint evaluation reads
 // with neighbours (I, D), the candidates, the bitmaps; then the rest
-constexpr int kPlaceOrder[B_COUNT] = {B_I, B_D, B_C, B_DIRTY, B_MARK, B_B, B_LIST, B_XS, B_E, B_R, B_K, B_A};
+constexpr int kPlaceOrder[B_COUNT] = {B_I, B_D, B_C, B_DIRTY, B_MARK, B_CLAIM, B_B, B_LIST, B_XS, B_E, B_R, B_K, B_A};
 
 // per-image stats: 0 sweeps, 1 fixpoint passes, 2 engine calls, 3 flips, then
 // thread-0 clock64 cycles: 4 prep (EDT/rank + E passes), 5 fixpoint passes,
@@ -82,6 +83,7 @@ struct KParams {
     int n, H, W, WW, nwords;
     int stride, plen;       // padded layout (see kPadRows)
     int pad;                // zero rows above / below the image (kPadRows)
+    int mwords;             // words of one 1-bit-per-word bitmap (dirty, each claim bitmap)
     int nstrips;            // strips = nblk * WW (a thread walks strips tid, tid + nthr, ...)
     int nblk, hb;           // strip mapping: row blocks per word column, rows per block
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
