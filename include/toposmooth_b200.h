@@ -147,11 +147,14 @@ int32_t ts_set_team_size(int32_t ctas);
  * (0 = automatic: 256 x 2 when the hot planes fit half an SM).  Returns the previous value. */
 int32_t ts_set_cta_threads(int32_t threads);
 
-/* Tuning / A-B: 1 (default) = ts_hasf_batch_host runs ONE fused launch that
- * starts while the input chunks are still being copied (stream memory
+/* Tuning / A-B of ts_hasf_batch_host: 1 (default) = the images are bit-packed
+ * on host threads (8x fewer bytes over the host link) and ONE fused launch
+ * starts while the packed chunks are still being copied (stream memory
  * operations gate each image on its chunk and each chunk's copy-back on its
- * images); 0 = the chunked pipeline of separate launches.  Returns the
- * previous value. */
+ * images); the results are unpacked on the host chunk by chunk; calls with
+ * keep / avoid planes stream the uint8 planes (as 2); 2 = streamed uint8
+ * chunks, no host packing; 0 = the chunked pipeline of separate launches.
+ * Returns the previous value. */
 int32_t ts_set_host_streaming(int32_t on);
 
 /* Tuning / A-B: 1 (default) = where eligible (one strip per thread, rows of

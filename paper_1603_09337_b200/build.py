@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libtoposmooth_b200.so")
 SOURCES = ["ts_hasf_8h.cu", "ts_hasf_4h.cu", "ts_hasf_8g.cu", "ts_hasf_4g.cu", "ts_hasf_8h256.cu",
-           "ts_hasf_4h256.cu", "ts_hasf.cu", "ts_edt.cu", "ts_ccl.cu", "ts_api.cu"]
+           "ts_hasf_4h256.cu", "ts_hasf.cu", "ts_edt.cu", "ts_ccl.cu", "ts_api.cu", "ts_hostpack.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
@@ -45,8 +45,9 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
     os.makedirs(obj_dir, exist_ok=True)
     procs = []
     for src in SOURCES:
-        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
+        extra = ["-Xcompiler", "-fopenmp"] if src.endswith(".cpp") else []   # host packing threads
+        cmd = [NVCC, *ARCH, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
@@ -63,7 +64,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
     if failed:
         raise RuntimeError(f"nvcc failed on {failed}")
     tmp = lib + ".tmp"
-    res = subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+    res = subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lgomp"], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc link failed for libtoposmooth_b200.so")

@@ -20,6 +20,7 @@
 #include "../../include/toposmooth_b200.h"
 #include "ts_common.cuh"
 #include "ts_internal.h"
+#include "ts_hostpack.h"
 
 namespace ts {
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream);
@@ -360,7 +361,7 @@ int check_fg(int32_t fg) {
 int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last,
                  int do_cut, int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, const int64_t *prio,
                  long long max_sweeps, cudaStream_t st, int64_t *stats_host, int *err_dev, int *team_out,
-                 const unsigned *ready = nullptr, unsigned *done = nullptr, int chunk = 1) {
+                 const unsigned *ready = nullptr, unsigned *done = nullptr, int chunk = 1, int packed_io = 0) {
     int rc;
     if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
     if (r_last > kMaxR)
@@ -439,6 +440,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.threads = pl.threads;
     p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
     p.fused = pl.fused ? 1 : 0;
+    p.packed_io = packed_io;
     p.ready = ready;
     p.done = done;
     p.chunk = chunk;
@@ -675,7 +677,150 @@ int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     return ok();
 }
 
-int32_t ts_set_host_streaming(int32_t on) { return g_streamed.exchange(on ? 1 : 0); }
+// Streamed host entry with host-side bit packing (no keep / avoid planes):
+// chunk k is packed on the host threads (8x fewer bytes over the link),
+// copied, flagged; the fused launch (packed_io) starts after chunk 0; every
+// chunk's packed result is copied back when its images are done and unpacked
+// on the host while the GPU finishes the later chunks.  Pinned staging
+// buffers are cached per process (one streamed call at a time holds them).
+std::mutex g_stage_mu;
+struct Stage {
+    uint32_t *in = nullptr, *out = nullptr;
+    size_t words = 0;
+} g_stage;
+
+// streams and events of the streamed entry, created once per device (held
+// under g_stage_mu for a call; creating them per call cost ~0.1 ms)
+struct HostCtx {
+    bool made = false;
+    cudaStream_t sin = nullptr, sout = nullptr, sc = nullptr;
+    cudaEvent_t ev0 = nullptr, ec = nullptr;
+    cudaEvent_t eo[kMaxChunks] = {};
+};
+HostCtx g_ctx[64];
+
+int host_ctx(int dev, HostCtx *&c) {
+    if (dev < 0 || dev >= 64) return fail(TS_ERR_UNSUPPORTED, "device index >= 64");
+    c = &g_ctx[dev];
+    if (c->made) return TS_OK;
+    TS_CUDA(cudaStreamCreateWithFlags(&c->sin, cudaStreamNonBlocking));
+    TS_CUDA(cudaStreamCreateWithFlags(&c->sout, cudaStreamNonBlocking));
+    TS_CUDA(cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking));
+    TS_CUDA(cudaEventCreateWithFlags(&c->ev0, cudaEventDisableTiming));
+    TS_CUDA(cudaEventCreateWithFlags(&c->ec, cudaEventDisableTiming));
+    for (int k = 0; k < kMaxChunks; ++k) TS_CUDA(cudaEventCreateWithFlags(&c->eo[k], cudaEventDisableTiming));
+    c->made = true;
+    return TS_OK;
+}
+
+int stage_reserve(size_t words) {
+    if (g_stage.words >= words) return TS_OK;
+    if (g_stage.in) cudaFreeHost(g_stage.in);
+    if (g_stage.out) cudaFreeHost(g_stage.out);
+    g_stage = Stage{};
+    TS_CUDA(cudaHostAlloc((void **)&g_stage.in, words * 4, cudaHostAllocDefault));
+    TS_CUDA(cudaHostAlloc((void **)&g_stage.out, words * 4, cudaHostAllocDefault));
+    g_stage.words = words;
+    return TS_OK;
+}
+
+int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w,
+                              int32_t r_max, int32_t fg, cudaStream_t user, const MemOps &mo) {
+    const int ww = (w + 31) / 32;
+    const size_t img = (size_t)h * w, wimg = (size_t)h * ww, words = (size_t)n * wimg;
+    int64_t chunk = std::max<int64_t>(1, (int64_t)((4u << 20) / std::max<size_t>(img, 1)));
+    chunk = std::max<int64_t>(chunk, (n + kMaxChunks - 1) / kMaxChunks);
+    const int nchunks = (int)((n + chunk - 1) / chunk);
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    int rc = stage_reserve(words);
+    if (rc) return rc;
+    uint32_t *hin = g_stage.in, *hout = g_stage.out;
+    // chunk 0 packed (and validated) before anything is enqueued
+    if (!pack_images(in_host, hin, std::min<int64_t>(chunk, n), h, w, ww))
+        return fail(TS_ERR_VALUE, "binary image pixels must be 0 or 1");   // grid.py:60-61
+    int dev = 0;
+    TS_CUDA(cudaGetDevice(&dev));
+    HostCtx *hc = nullptr;
+    if ((rc = host_ctx(dev, hc))) return rc;
+    uint32_t *d = nullptr;
+    int *err = nullptr;
+    TS_CUDA(cudaMallocAsync((void **)&d, words * 4 * 2, user));
+    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
+    TS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), user));
+    unsigned *flags = take_flags(dev);
+    if (!flags) return fail(TS_ERR_CUDA, "cudaMalloc(chunk flags)");
+    TS_CUDA(cudaMemsetAsync(flags, 0, 2 * nchunks * sizeof(unsigned), user));
+    uint32_t *din = d, *dout = d + words;
+    unsigned *ready = flags, *done = flags + nchunks;
+    cudaStream_t sin = hc->sin, sout = hc->sout, sc = hc->sc;
+    cudaEvent_t ev0 = hc->ev0, ec = hc->ec;
+    cudaEvent_t *eo = hc->eo;
+    cudaError_t e = cudaEventRecord(ev0, user);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, ev0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev0, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev0, 0);
+    int mrc = 0;
+    bool bad = false;
+    auto send = [&](int k) {   // chunk k (already packed): copy, then flag
+        const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+        if (!bad) e = cudaMemcpyAsync(din + i0 * wimg, hin + i0 * wimg, cnt * wimg * 4, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) mrc = mo.write(sin, (unsigned long long)(uintptr_t)(ready + k), 1u, kWriteDefault);
+    };
+    if (e == cudaSuccess) send(0);
+    if (e == cudaSuccess && mrc == 0)
+        rc = fused_launch(MODE_HASF, reinterpret_cast<const uint8_t *>(din), reinterpret_cast<uint8_t *>(dout), n, h,
+                          w, 1, r_max, 1, 1, fg, nullptr, nullptr, nullptr, -1, sc, nullptr, err, nullptr, ready, done,
+                          (int)chunk, 1);
+    const bool launched = e == cudaSuccess && mrc == 0 && rc == TS_OK;
+    if (launched) {
+        for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
+            const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+            mrc = mo.wait(sout, (unsigned long long)(uintptr_t)(done + k), (unsigned)cnt, kWaitGeq);
+            if (mrc == 0)
+                e = cudaMemcpyAsync(hout + i0 * wimg, dout + i0 * wimg, cnt * wimg * 4, cudaMemcpyDeviceToHost, sout);
+            if (e == cudaSuccess) e = cudaEventRecord(eo[k], sout);
+        }
+        // the rest of the input: pack chunk k while chunk k-1 is on the link
+        // (after a bad chunk the flags are still raised so the launch drains)
+        for (int k = 1; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
+            const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+            if (!bad && !pack_images(in_host + i0 * img, hin + i0 * wimg, cnt, h, w, ww)) bad = true;
+            send(k);
+        }
+        // results: unpack chunk k as soon as its copy-back finished
+        for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0 && !bad; ++k) {
+            const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+            e = cudaEventSynchronize(eo[k]);
+            if (e == cudaSuccess) unpack_images(hout + i0 * wimg, out_host + i0 * img, cnt, h, w, ww);
+        }
+    }
+    cudaEventRecord(ec, sc);
+    cudaStreamWaitEvent(user, ec, 0);
+    if (launched) {
+        cudaEvent_t el = eo[nchunks - 1];
+        if (el) cudaStreamWaitEvent(user, el, 0);
+    }
+    int herr = 0;
+    cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, user);
+    const std::string keep_msg = g_err;
+    cudaFreeAsync(d, user);
+    cudaFreeAsync(err, user);
+    cudaError_t se = cudaStreamSynchronize(user);
+    give_flags(dev, flags);
+    if (rc) {
+        g_err = keep_msg;
+        return rc;
+    }
+    if (mrc) return fail(TS_ERR_CUDA, "stream memory operation failed (code " + std::to_string(mrc) + ")");
+    if (e != cudaSuccess) return cuda_fail(e, "streamed host path");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
+    if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
+    if (bad) return fail(TS_ERR_VALUE, "binary image pixels must be 0 or 1");   // grid.py:60-61
+    if (herr) return device_error(herr, MODE_HASF);
+    return ok();
+}
+
+int32_t ts_set_host_streaming(int32_t on) { return g_streamed.exchange(on < 0 ? 0 : (on > 2 ? 2 : on)); }
 
 int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
 
@@ -694,8 +839,11 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     const size_t img = (size_t)h * w, bytes = (size_t)n * img;
     const bool big = (long long)h * w > 1024LL * 1024;   // team-sized images: one chunk
     const MemOps &mo = memops();
-    if (!big && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR)
+    if (!big && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR) {
+        if (!keep_host && !avoid_host && g_streamed.load() == 1)
+            return hasf_host_streamed_packed(in_host, out_host, n, h, w, r_max, fg, user, mo);
         return hasf_host_streamed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);
+    }
     const int nchunks = big ? 1 : (int)std::min<int64_t>(n, 4);
     const int ncs = 3;   // compute streams
     const int64_t per = (n + nchunks - 1) / nchunks;

@@ -1799,7 +1799,7 @@ __device__ __forceinline__ void run_stage(const View &v, const Img &gt, int r, b
 
 // image prologue: clear planes, pack inputs, validate (all team threads)
 template <bool HOT>
-__device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size_t pix) {
+__device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size_t pix, int img) {
     const KParams &p = *pp;
     const Img g = make_img<HOT>(v);
     const int tid = g.tid, nthr = g.nthr;
@@ -1818,7 +1818,12 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
         g.flags[0] = g.flags[1] = g.flags[2] = 0;
     }
     team_sync(g);
-    pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
+    if (p.packed_io) {   // host-packed bit rows (validated on the host)
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(p.in) + (size_t)img * g.H * g.WW;
+        for_strip(g, [&](int y, int x, int q) { g.I[q] = src[(size_t)y * g.WW + x]; });
+    } else {
+        pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
+    }
     if (p.mode == MODE_THIN || p.mode == MODE_THICKEN) {
         pack_plane(p.keep + pix, g.B, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
     } else {
@@ -1844,9 +1849,12 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
 }
 
 template <bool HOT>
-__device__ __noinline__ void store_image_nl(const View v, uint8_t *out) {
+__device__ __noinline__ void store_image_nl(const View v, uint8_t *out, uint32_t *out_bits) {
     const Img g = make_img<HOT>(v);
-    unpack_plane(g.I, out, g);
+    if (out_bits)   // packed output: bit rows, copied back and unpacked by the host
+        for_strip(g, [&](int y, int x, int q) { out_bits[(size_t)y * g.WW + x] = g.I[q]; });
+    else
+        unpack_plane(g.I, out, g);
 }
 
 // HOT: one CTA per image, hot planes in shared memory.  !HOT: a team of
@@ -1943,7 +1951,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.bstat[0] = sh.bstat[1] = sh.bstat[2] = sh.bstat[3] = 0;
             sh.xstat[0] = sh.xstat[1] = sh.xstat[2] = sh.xstat[3] = 0;
         }
-        load_image_nl<HOT>(v, &p, pix);
+        load_image_nl<HOT>(v, &p, pix, img);
         team_sync(gk);
 
         Stats st{};
@@ -1969,7 +1977,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             engine<FG, HOT>(v, t, p.max_sweeps, sh, cur, p.err, st, pc);
         }
 
-        store_image_nl<HOT>(v, p.out + pix);
+        store_image_nl<HOT>(v, p.out + pix,
+                            p.packed_io ? reinterpret_cast<uint32_t *>(p.out) + (size_t)img * p.H * p.WW : nullptr);
         if (lead && p.stats) {
             long long *sp = p.stats + (size_t)img * kStatFields;
             sp[0] = st.sweeps;

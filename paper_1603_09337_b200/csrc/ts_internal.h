@@ -107,6 +107,7 @@ struct KParams {
     unsigned *done;
     int chunk;
     int fused;              // 1: fused prep + E-pass allowed (the planner left out the R planes)
+    int packed_io;          // 1: in / out are [n][H][WW] uint32 bit rows (host-packed, validated)
     int *err;               // first error code (atomicCAS from 0)
     long long *stats;       // [n][kStatFields] (or null), see kStatFields
 };

@@ -329,12 +329,14 @@ def test_fused_and_two_phase_prep_vs_oracle(fused):
         lib.ts_set_fused_prep(old)
 
 
-@pytest.mark.parametrize("streaming", [1, 0])
+@pytest.mark.parametrize("streaming", [1, 2, 0])
 def test_streamed_host_entry_vs_device_path(streaming):
     """ts_hasf_batch_host: one launch gated on streamed input chunks (and
-    chunk-gated copy-back), or the chunked pipeline -- against the
-    device-resident path, for batch sizes around the chunk size (16 images of
-    512^2), a single image, other shapes and keep / avoid constraints."""
+    chunk-gated copy-back) with host bit packing (1) or uint8 chunks (2), or
+    the chunked pipeline (0) -- against the device-resident path, for batch
+    sizes around the chunk size (16 images of 512^2), a single image, other
+    shapes, ragged widths, keep / avoid constraints and invalid pixels (also
+    in a chunk copied after the launch started)."""
     lib = _lib.load()
     old = lib.ts_set_host_streaming(streaming)
     try:
@@ -361,6 +363,16 @@ def test_streamed_host_entry_vs_device_path(streaming):
         bad = imgs.copy()
         bad[2, 5, 5] = 7
         rc = lib.ts_hasf_batch_host(bad.ctypes.data, out.ctypes.data, 5, 100, 96, 3, 8, None, None, stream)
+        assert rc == _lib.TS_ERR_VALUE and b"0 or 1" in lib.ts_last_error()
+        for (h, w) in ((37, 45), (64, 33), (20, 300)):   # ragged widths (partial last word)
+            imgs = np.stack([random_image(rng, h, w, 0.5) for _ in range(7)])
+            out = np.zeros_like(imgs)
+            _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, 7, h, w, 2, 4, None, None, stream))
+            assert np.array_equal(out, O.hasf_batch(imgs, 2, 4, threads=4)), (streaming, h, w)
+        big = W.config_batch("c1", 1300, 40)
+        big[35, 100, 100] = 3   # lands in the third 16-image chunk
+        hout = np.zeros_like(big)
+        rc = lib.ts_hasf_batch_host(big.ctypes.data, hout.ctypes.data, 40, 512, 512, 5, 8, None, None, stream)
         assert rc == _lib.TS_ERR_VALUE and b"0 or 1" in lib.ts_last_error()
     finally:
         lib.ts_set_host_streaming(old)
