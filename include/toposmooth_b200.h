@@ -50,7 +50,7 @@ int ts_max_radius(void);
 /* HASF: alternate homotopic cutting and filling at radii 1..r_max.
  * Replaces hasf(img, SmoothingConfig(r_max, adj, keep, avoid)) and smooth(img, r_max)
  * (smoothing.py:187-217).  keep_dev / avoid_dev: [n][h][w] constraint images or
- * NULL.  stats_host: NULL or int64[n*32] receiving per image: sweeps, fixpoint
+ * NULL.  stats_host: NULL or int64[n*36] receiving per image: sweeps, fixpoint
  * passes, engine calls, flips, then SM clock cycles spent in prep (clamped
  * EDT + precedence masks), fixpoint passes, apply+re-examination, in total,
  * and a breakdown by sweep size (fields 8-14; 15 reserved). */

@@ -1006,7 +1006,8 @@ struct Shared {
     long long dtime[4];  // stats: dense pass-1 / collect / list-pass cycles, listed words
     long long sstat[4];  // stats: list sweeps (33..512 words) count / cycles, (> 512) count / cycles
     long long bstat[4];  // stats, list sweeps > 512 words: list-build / sweep / re-examination cycles, list builds
-    long long xstat[4];  // stats: tiny regimes (incl. list build and barriers) cycles / count; 2-3 spare
+    long long xstat[4];  // stats: tiny regimes (incl. list build and barriers) cycles / count; engine; stage
+    long long ystat[4];  // stats: engine prologue, loop tops, epilogue cycles; sweeps-loop iterations
 };
 
 // per-team control block in global memory (teams of G > 1 CTAs)
@@ -1082,7 +1083,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
 }
 
 template <bool HOT, int R>
-__device__ __noinline__ int prep_nl(const View v, bool thin, int xmode, bool save_xs) {
+__device__ __noinline__ int prep_nl(const View &v, bool thin, int xmode, bool save_xs) {
     const Img g = make_img<HOT>(v);
     return prep_rank<R>(g, thin, xmode, save_xs);
 }
@@ -1104,7 +1105,7 @@ __device__ __forceinline__ int prep_dispatch_v(int r, const View &v, bool thin, 
 }
 
 template <int FG, bool HOT, int S>
-__device__ __noinline__ void epass_nl(const View v, int t, int cur) {
+__device__ __noinline__ void epass_nl(const View &v, int t, int cur) {
     const Img g = make_img<HOT>(v);
     epass_ranks<FG, S>(g, t, &g.sh->counters[cur]);
 }
@@ -1124,7 +1125,7 @@ __device__ __forceinline__ void epass_dispatch_v(const View &v, int S, int t, in
 static_assert(kMaxSlices <= 7, "epass_dispatch covers up to 7 rank slices");
 
 template <int FG, bool HOT, int R>
-__device__ __noinline__ void prep_fused_nl(const View v, bool thin, int xmode, bool save_xs, int t, int cur) {
+__device__ __noinline__ void prep_fused_nl(const View &v, bool thin, int xmode, bool save_xs, int t, int cur) {
     const Img g = make_img<HOT>(v);
     prep_fused<FG, R>(g, thin, xmode, save_xs, t, &g.sh->counters[cur]);
 }
@@ -1150,7 +1151,7 @@ __device__ __forceinline__ bool prep_fused_dispatch_v(int r, const View &v, bool
 static_assert(kFusedMaxR == 8, "prep_fused_dispatch_v covers radii 1..8");
 
 template <int FG, bool HOT>
-__device__ __noinline__ void epass_prio_nl(const View v, const int64_t *prio, int t, int cur) {
+__device__ __noinline__ void epass_prio_nl(const View &v, const int64_t *prio, int t, int cur) {
     const Img g = make_img<HOT>(v);
     epass_prio<FG>(g, prio, t, &g.sh->counters[cur]);
 }
@@ -1177,7 +1178,7 @@ struct TinyOut {
 };
 
 template <int FG, bool HOT>
-__device__ __noinline__ TinyOut tiny_sweeps(const View v, int t, int cur, long long budget, bool timing) {
+__device__ __noinline__ TinyOut tiny_sweeps(const View &v, int t, int cur, long long budget, bool timing) {
     const Img g = make_img<HOT>(v);
     const int lane = threadIdx.x & 31;
     Shared &sh = *g.sh;
@@ -1546,13 +1547,13 @@ __device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long 
 
 // the sweeps as separate functions: each gets its own register allocation
 template <int FG, bool HOT>
-__device__ __noinline__ SweepOut dense_sweep_nl(const View v, long long cap, int pc, bool timing) {
+__device__ __noinline__ SweepOut dense_sweep_nl(const View &v, long long cap, int pc, bool timing) {
     const Img g = make_img<HOT>(v);
     return dense_sweep<FG, HOT>(g, cap, pc, timing);
 }
 
 template <int FG, bool HOT>
-__device__ __noinline__ SweepOut sparse_sweep_nl(const View v, int n, long long cap, int pc) {
+__device__ __noinline__ SweepOut sparse_sweep_nl(const View &v, int n, long long cap, int pc) {
     const Img g = make_img<HOT>(v);
     return sparse_sweep<FG>(g, n, cap, pc);
 }
@@ -1599,13 +1600,16 @@ struct EngineIO {   // engine state carried across calls (block-uniform)
 };
 
 template <int FG, bool HOT>
-__device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long max_sweeps, int *err, bool timing,
+__device__ TS_ENGINE_INLINE EngineIO engine_nl(const View &v, int t, long long max_sweeps, int *err, bool timing,
                                            EngineIO io) {
     (void)err;
+    const long long ty0 = timing ? clock64() : 0;
     const Img g = make_img<HOT>(v);
     Shared &sh = *g.sh;
     const int tid = g.tid;
     volatile int *vcount = sh.counters;
+    long long tyl = timing ? clock64() : 0;   // start of the current loop top
+    if (timing && tid == 0) sh.ystat[0] += tyl - ty0;
     int cur = io.cur, pc = io.pc;
     Stats st{};
     st.timing = timing;
@@ -1624,6 +1628,10 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
             break;
         }
         const long long tj0 = st.timing ? clock64() : 0;
+        if (st.timing && tid == 0) {
+            sh.ystat[1] += tj0 - tyl;
+            sh.ystat[3] += 1;
+        }
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
         const bool tiny = g.G == 1 && n <= 32;   // warp-resident regime (needs the list)
         const bool dense = n > g.dense_min && !tiny;
@@ -1675,6 +1683,7 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
                 if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
                 break;
             }
+            if (st.timing) tyl = clock64();
             continue;
         }
         SweepOut o;
@@ -1731,8 +1740,10 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
                     sh.bstat[2] += tj2 - tj1;
                 }
             }
+            tyl = clock64();
         }
     }
+    const long long tye = timing ? clock64() : 0;
     io.cur = cur;
     io.pc = pc;
     io.sweeps += sweeps;
@@ -1746,6 +1757,7 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View v, int t, long long ma
     io.cyc_dense += st.cyc_dense;
     io.n_dense += st.n_dense;
     io.pass_dense += st.pass_dense;
+    if (timing && tid == 0) sh.ystat[2] += clock64() - tye;
     return io;
 }
 
@@ -1794,12 +1806,18 @@ __device__ __forceinline__ void run_stage(const View &v, const Img &gt, int r, b
     }
     team_sync(gt);
     if (st.timing) st.cyc_prep += clock64() - tp0;
+    const long long te0 = st.timing ? clock64() : 0;
     engine<FG, HOT>(v, thin ? 1 : 0, -1, sh, cur, err, st, pc);
+    if (st.timing && gt.tid == 0) {
+        const long long te1 = clock64();
+        sh.xstat[2] += te1 - te0;   // whole engine call
+        sh.xstat[3] += te1 - tp0;   // whole stage
+    }
 }
 
 // image prologue: clear planes, pack inputs, validate (all team threads)
 template <bool HOT>
-__device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size_t pix, int img) {
+__device__ __noinline__ void load_image_nl(const View &v, const KParams *pp, size_t pix, int img) {
     const KParams &p = *pp;
     const Img g = make_img<HOT>(v);
     const int tid = g.tid, nthr = g.nthr;
@@ -1849,7 +1867,7 @@ __device__ __noinline__ void load_image_nl(const View v, const KParams *pp, size
 }
 
 template <bool HOT>
-__device__ __noinline__ void store_image_nl(const View v, uint8_t *out, uint32_t *out_bits) {
+__device__ __noinline__ void store_image_nl(const View &v, uint8_t *out, uint32_t *out_bits) {
     const Img g = make_img<HOT>(v);
     if (out_bits)   // packed output: bit rows, copied back and unpacked by the host
         for_strip(g, [&](int y, int x, int q) { out_bits[(size_t)y * g.WW + x] = g.I[q]; });
@@ -1871,48 +1889,53 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     auto buf = [&](int b) -> uint32_t * { return ((p.smem_mask >> b) & 1u) ? smem + p.off[b] : cta + p.off[b]; };
     TeamCtl *tc = G == 1 ? nullptr : reinterpret_cast<TeamCtl *>(p.tctl) + team;
     Shared *shp = G == 1 ? &sh_local : &tc->sh;
-    View v;
+    View vl;   // built by every thread, published in shared memory: the noinline
+               // phases take it by reference (no per-call copy to local memory)
     if constexpr (HOT) {
         const unsigned long long base = (unsigned long long)__cvta_generic_to_shared(smem);
-        v.I = base + 4ull * p.off[B_I];
-        v.D = base + 4ull * p.off[B_D];
-        v.C = base + 4ull * p.off[B_C];
-        v.dirty = base + 4ull * p.off[B_DIRTY];
-        v.mark = base + 4ull * p.off[B_MARK];
+        vl.I = base + 4ull * p.off[B_I];
+        vl.D = base + 4ull * p.off[B_D];
+        vl.C = base + 4ull * p.off[B_C];
+        vl.dirty = base + 4ull * p.off[B_DIRTY];
+        vl.mark = base + 4ull * p.off[B_MARK];
     } else {
-        v.I = (unsigned long long)buf(B_I);
-        v.D = (unsigned long long)buf(B_D);
-        v.C = (unsigned long long)buf(B_C);
-        v.dirty = (unsigned long long)buf(B_DIRTY);
-        v.mark = (unsigned long long)buf(B_MARK);
+        vl.I = (unsigned long long)buf(B_I);
+        vl.D = (unsigned long long)buf(B_D);
+        vl.C = (unsigned long long)buf(B_C);
+        vl.dirty = (unsigned long long)buf(B_DIRTY);
+        vl.mark = (unsigned long long)buf(B_MARK);
     }
-    v.B = buf(B_B);
-    v.claim = buf(B_CLAIM);
-    v.mw = p.mwords;
-    v.list = buf(B_LIST);
-    v.E = buf(B_E);
-    v.XS = buf(B_XS);
-    v.R = buf(B_R);
-    v.K = buf(B_K);
-    v.A = buf(B_A);
-    v.H = p.H;
-    v.W = p.W;
-    v.WW = p.WW;
-    v.S = p.stride;
-    v.plen = p.plen;
-    v.org = p.pad * p.stride + 1;
-    v.nblk = p.nblk;
-    v.hb = p.hb;
-    v.nstrips = p.nstrips;
-    v.fused = p.fused;
-    v.dense_min = p.dense_min;
-    v.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
-    v.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;
-    v.G = G;
-    v.rank = rank;
-    v.bar = tc ? tc->bar : nullptr;
-    v.flags = tc ? tc->flags : nullptr;
-    v.err = p.err;
+    vl.B = buf(B_B);
+    vl.claim = buf(B_CLAIM);
+    vl.mw = p.mwords;
+    vl.list = buf(B_LIST);
+    vl.E = buf(B_E);
+    vl.XS = buf(B_XS);
+    vl.R = buf(B_R);
+    vl.K = buf(B_K);
+    vl.A = buf(B_A);
+    vl.H = p.H;
+    vl.W = p.W;
+    vl.WW = p.WW;
+    vl.S = p.stride;
+    vl.plen = p.plen;
+    vl.org = p.pad * p.stride + 1;
+    vl.nblk = p.nblk;
+    vl.hb = p.hb;
+    vl.nstrips = p.nstrips;
+    vl.fused = p.fused;
+    vl.dense_min = p.dense_min;
+    vl.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
+    vl.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;
+    vl.G = G;
+    vl.rank = rank;
+    vl.bar = tc ? tc->bar : nullptr;
+    vl.flags = tc ? tc->flags : nullptr;
+    vl.err = p.err;
+    __shared__ View v_shared;
+    if (threadIdx.x == 0) v_shared = vl;
+    __syncthreads();
+    const View &v = v_shared;
     const Img gk = make_img<HOT>(v);   // team / sync view for this function
     Shared &sh = *shp;
     const bool has_k = p.keep != nullptr, has_a = p.avoid != nullptr;
@@ -1950,6 +1973,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.sstat[0] = sh.sstat[1] = sh.sstat[2] = sh.sstat[3] = 0;
             sh.bstat[0] = sh.bstat[1] = sh.bstat[2] = sh.bstat[3] = 0;
             sh.xstat[0] = sh.xstat[1] = sh.xstat[2] = sh.xstat[3] = 0;
+            sh.ystat[0] = sh.ystat[1] = sh.ystat[2] = sh.ystat[3] = 0;
         }
         load_image_nl<HOT>(v, &p, pix, img);
         team_sync(gk);
@@ -2002,6 +2026,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
                 sp[20 + k] = *reinterpret_cast<volatile long long *>(&sh.dtime[k]);
                 sp[24 + k] = *reinterpret_cast<volatile long long *>(&sh.bstat[k]);
                 sp[28 + k] = *reinterpret_cast<volatile long long *>(&sh.xstat[k]);
+                sp[32 + k] = *reinterpret_cast<volatile long long *>(&sh.ystat[k]);
             }
         }
         team_sync(gk);

@@ -55,8 +55,10 @@ constexpr int kPlaceOrder[B_COUNT] = {B_I, B_D, B_C, B_DIRTY, B_MARK, B_CLAIM, B
 // of > 512 words: count, cycles; 20-23 dense sweeps: cycles of the strip-walk pass, of the list collection
 // (incl. barriers), of the compacted passes; listed words; 24-27 list sweeps
 // of > 512 words: list-build, sweep, re-examination cycles, list builds;
-// 28-29 tiny regimes: cycles (incl. list build and barriers), count; 30-31 spare
-constexpr int kStatFields = 32;
+// 28-29 tiny regimes: cycles (incl. list build and barriers), count; 30 whole
+// engine calls, 31 whole stages (cycles); 32-35 engine prologue, loop tops,
+// epilogue cycles, sweep-loop iterations
+constexpr int kStatFields = 36;
 
 enum Mode : int { MODE_HASF = 0, MODE_THIN = 1, MODE_THICKEN = 2 };
 

@@ -131,7 +131,7 @@ def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=Non
         if t is not None and tuple(t.shape) != (n, h, w):
             raise ValueError(f"{name} constraint shape {tuple(t.shape)} != batch shape {(n, h, w)}")
     out = torch.empty_like(x)
-    st = np.zeros((n, 32), np.int64) if stats else None
+    st = np.zeros((n, 36), np.int64) if stats else None
     check(load().ts_hasf_batch(x.data_ptr(), out.data_ptr(), n, h, w, r_max, adj.fg, D.ptr(k), D.ptr(a),
                                D.stream_ptr(), None if st is None else st.ctypes.data))
     res = out.cpu().numpy() if is_numpy else out

@@ -198,7 +198,7 @@ def test_hasf_batch_vs_oracle_c1_c4_samples():
 def test_stats_are_reported():
     imgs = W.config_batch("c0", 0, 1)
     out, st = P.hasf_batch(imgs, 3, stats=True)
-    assert st.shape == (1, 32) and st[0, 7] >= st[0, 4] + st[0, 5] > 0
+    assert st.shape == (1, 36) and st[0, 7] >= st[0, 4] + st[0, 5] > 0
     assert st[0, 2] == 12 and st[0, 0] > 0 and st[0, 1] >= st[0, 0] and st[0, 3] > 0
 
 

@@ -72,7 +72,7 @@ def main():
                     "cyc_tiny": m[8], "n_tiny": m[9], "pass_tiny": m[10], "cyc_dense": m[11], "n_dense": m[12],
                     "pass_dense": m[13], "cyc_rank": m[14], "evals": m[15],
                                         "n_sp_small": m[16], "cyc_sp_small": m[17], "n_sp_big": m[18], "cyc_sp_big": m[19],
-                    "x_tiny": m[28], "n_tinyreg": m[29], "b_build": m[24], "b_sweep": m[25], "b_rebuild": m[26], "n_build": m[27],
+                    "x_tiny": m[28], "n_tinyreg": m[29], "y_pro": m[32], "y_top": m[33], "y_epi": m[34], "y_iter": m[35], "x_engine": m[30], "x_stage": m[31], "b_build": m[24], "b_sweep": m[25], "b_rebuild": m[26], "n_build": m[27],
                     "cyc_dpass1": m[20], "cyc_dcollect": m[21], "cyc_dlist": m[22], "d_listed": m[23]})
     print(json.dumps(res, default=float))
 
