@@ -1407,22 +1407,88 @@ __device__ __forceinline__ void claim_chg(const Img &g, int p, uint32_t chg, uin
     }
 }
 
+// the same claims, returning the newly claimed words as a mask over qs[]
+// (the caller appends them, aggregated per warp)
+__device__ __forceinline__ uint32_t claim_chg_mask(const Img &g, int p, uint32_t chg, uint4 e0, uint4 e1, uint32_t *Q,
+                                                   int (&qs)[8]) {
+    const int S = g.S;
+    uint32_t firsts = 0;   // bit k: qs[k] newly claimed here
+    auto claim = [&](int k, int q) {
+        qs[k] = q;
+        if (g.C[q] == 0u) return;
+        const uint32_t bit = 1u << (q & 31);
+        if (!(atomicOr(&Q[q >> 5], bit) & bit)) firsts |= 1u << k;
+    };
+    const uint32_t lNW = ~e0.x, lN = ~e0.y, lNE = ~e0.z, lW = ~e0.w;   // "that neighbour is later"
+    const uint32_t lE = ~e1.x, lSW = ~e1.y, lS = ~e1.z, lSE = ~e1.w;
+    if (chg & (lN | (lNW & ~1u) | (lNE & 0x7FFFFFFFu))) claim(0, p - S);
+    if (chg & (lS | (lSW & ~1u) | (lSE & 0x7FFFFFFFu))) claim(1, p + S);
+    if (chg & 1u) {
+        if (lNW & 1u) claim(2, p - S - 1);
+        if (lW & 1u) claim(3, p - 1);
+        if (lSW & 1u) claim(4, p + S - 1);
+    }
+    if (chg >> 31) {
+        if (lNE >> 31) claim(5, p - S + 1);
+        if (lE >> 31) claim(6, p + 1);
+        if (lSE >> 31) claim(7, p + S + 1);
+    }
+    return firsts;
+}
+
 // pass j of a sweep's compacted phase: evaluate list (n words, in-word chains
 // resolved at once), claims into bitmap Q -> next; Qclear (the next pass's
-// bitmap, idle now) is cleared on the way
+// bitmap, idle now) is cleared on the way.  Single-CTA images append per
+// claim (shared-memory counter); teams aggregate the appends per warp (one
+// atomic on the team's global counter per warp and step: per-claim global
+// atomics on one address serialised c3 by 25%).
 template <int FG>
 __device__ __forceinline__ void claim_pass(const Img &g, const uint32_t *list, int n, uint32_t *Q, uint32_t *Qclear,
                                            uint32_t *next, int *ncount, int &evals) {
     for (int q = g.tid; q < g.mw; q += g.nthr) Qclear[q] = 0u;
-    for (int sl = g.tid; sl < n; sl += g.nthr) {
-        WordEval a;
-        load_eval(g, (int)list[sl], a);
-        const uint32_t nd = solve_eval<FG>(a);
-        ++evals;
-        if (nd != a.old) {
-            g.D[a.p] = nd;
-            claim_chg(g, a.p, nd ^ a.old, a.e0, a.e1, Q, next, ncount);
+    if (g.G == 1) {
+        for (int sl = g.tid; sl < n; sl += g.nthr) {
+            WordEval a;
+            load_eval(g, (int)list[sl], a);
+            const uint32_t nd = solve_eval<FG>(a);
+            ++evals;
+            if (nd != a.old) {
+                g.D[a.p] = nd;
+                claim_chg(g, a.p, nd ^ a.old, a.e0, a.e1, Q, next, ncount);
+            }
         }
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int s0 = g.tid - lane; s0 < n; s0 += g.nthr) {   // warp-uniform trip count
+        const int sl = s0 + lane;
+        uint32_t firsts = 0;
+        int qs[8];
+        if (sl < n) {
+            WordEval a;
+            load_eval(g, (int)list[sl], a);
+            const uint32_t nd = solve_eval<FG>(a);
+            ++evals;
+            if (nd != a.old) {
+                g.D[a.p] = nd;
+                firsts = claim_chg_mask(g, a.p, nd ^ a.old, a.e0, a.e1, Q, qs);
+            }
+        }
+        const int cnt = __popc(firsts);
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int base = 0;
+        if (lane == 31) base = atomicAdd(ncount, tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if ((firsts >> k) & 1u) next[base++] = (uint32_t)qs[k];
     }
 }
 
