@@ -995,6 +995,11 @@ struct Stats {
     bool timing;
 };
 
+struct EngineIO {   // engine statistics of the current image, accumulated by team thread 0
+    long long sweeps, passes, calls;
+    long long cyc_jacobi, cyc_update, cyc_tiny, n_tiny, pass_tiny, cyc_dense, n_dense, pass_dense;
+};
+
 struct Shared {
     int img;
     int counters[2];
@@ -1008,6 +1013,7 @@ struct Shared {
     long long bstat[4];  // stats, list sweeps > 512 words: list-build / sweep / re-examination cycles, list builds
     long long xstat[4];  // stats: tiny regimes (incl. list build and barriers) cycles / count; engine; stage
     long long ystat[4];  // stats: engine prologue, loop tops, epilogue cycles; sweeps-loop iterations
+    EngineIO eio;        // engine statistics (returned through here, not by value: no local-memory copies)
 };
 
 // per-team control block in global memory (teams of G > 1 CTAs)
@@ -1659,15 +1665,10 @@ __device__ __forceinline__ void discard_sweep(const Img &g, int n, bool list_ok)
 #ifndef TS_ENGINE_INLINE
 #define TS_ENGINE_INLINE __noinline__
 #endif
-struct EngineIO {   // engine state carried across calls (block-uniform)
-    int cur, pc;
-    long long sweeps, passes, calls;
-    long long cyc_jacobi, cyc_update, cyc_tiny, n_tiny, pass_tiny, cyc_dense, n_dense, pass_dense;
-};
 
 template <int FG, bool HOT>
-__device__ TS_ENGINE_INLINE EngineIO engine_nl(const View &v, int t, long long max_sweeps, int *err, bool timing,
-                                           EngineIO io) {
+__device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_sweeps, int *err, bool timing, int cur0,
+                                           int pc0) {
     (void)err;
     const long long ty0 = timing ? clock64() : 0;
     const Img g = make_img<HOT>(v);
@@ -1676,7 +1677,7 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View &v, int t, long long m
     volatile int *vcount = sh.counters;
     long long tyl = timing ? clock64() : 0;   // start of the current loop top
     if (timing && tid == 0) sh.ystat[0] += tyl - ty0;
-    int cur = io.cur, pc = io.pc;
+    int cur = cur0, pc = pc0;
     Stats st{};
     st.timing = timing;
     long long sweeps = 0;
@@ -1810,49 +1811,32 @@ __device__ TS_ENGINE_INLINE EngineIO engine_nl(const View &v, int t, long long m
         }
     }
     const long long tye = timing ? clock64() : 0;
-    io.cur = cur;
-    io.pc = pc;
-    io.sweeps += sweeps;
-    io.passes += st.passes;
-    io.calls += 1;
-    io.cyc_jacobi += st.cyc_jacobi;
-    io.cyc_update += st.cyc_update;
-    io.cyc_tiny += st.cyc_tiny;
-    io.n_tiny += st.n_tiny;
-    io.pass_tiny += st.pass_tiny;
-    io.cyc_dense += st.cyc_dense;
-    io.n_dense += st.n_dense;
-    io.pass_dense += st.pass_dense;
-    if (timing && tid == 0) sh.ystat[2] += clock64() - tye;
-    return io;
+    if (tid == 0) {
+        EngineIO &io = sh.eio;
+        io.sweeps += sweeps;
+        io.passes += st.passes;
+        io.calls += 1;
+        io.cyc_jacobi += st.cyc_jacobi;
+        io.cyc_update += st.cyc_update;
+        io.cyc_tiny += st.cyc_tiny;
+        io.n_tiny += st.n_tiny;
+        io.pass_tiny += st.pass_tiny;
+        io.cyc_dense += st.cyc_dense;
+        io.n_dense += st.n_dense;
+        io.pass_dense += st.pass_dense;
+        if (timing) sh.ystat[2] += clock64() - tye;
+    }
+    return make_int2(cur, pc);
 }
 
 template <int FG, bool HOT>
 __device__ __forceinline__ void engine(const View &v, int t, long long max_sweeps, Shared &sh, int &cur, int *err,
                                        Stats &st, int &pc) {
-    EngineIO io{};
-    io.cur = cur;
-    io.pc = pc;
-#ifdef TS_PROF2
-    const long long te0 = clock64();
-#endif
-    io = engine_nl<FG, HOT>(v, t, max_sweeps, err, st.timing, io);
-#ifdef TS_PROF2
-    st.cyc_rank += clock64() - te0;   // profiling build: whole engine calls
-#endif
-    cur = io.cur;
-    pc = io.pc;
-    st.sweeps += io.sweeps;
-    st.passes += io.passes;
-    st.calls += io.calls;
-    st.cyc_jacobi += io.cyc_jacobi;
-    st.cyc_update += io.cyc_update;
-    st.cyc_tiny += io.cyc_tiny;
-    st.n_tiny += io.n_tiny;
-    st.pass_tiny += io.pass_tiny;
-    st.cyc_dense += io.cyc_dense;
-    st.n_dense += io.n_dense;
-    st.pass_dense += io.pass_dense;
+    (void)sh;
+    (void)st;
+    const int2 r = engine_nl<FG, HOT>(v, t, max_sweeps, err, st.timing, cur, pc);
+    cur = r.x;
+    pc = r.y;
 }
 
 template <int FG, bool HOT>
@@ -2040,6 +2024,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.bstat[0] = sh.bstat[1] = sh.bstat[2] = sh.bstat[3] = 0;
             sh.xstat[0] = sh.xstat[1] = sh.xstat[2] = sh.xstat[3] = 0;
             sh.ystat[0] = sh.ystat[1] = sh.ystat[2] = sh.ystat[3] = 0;
+            sh.eio = EngineIO{};
         }
         load_image_nl<HOT>(v, &p, pix, img);
         team_sync(gk);
@@ -2071,20 +2056,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
                             p.packed_io ? reinterpret_cast<uint32_t *>(p.out) + (size_t)img * p.H * p.WW : nullptr);
         if (lead && p.stats) {
             long long *sp = p.stats + (size_t)img * kStatFields;
-            sp[0] = st.sweeps;
-            sp[1] = st.passes;
-            sp[2] = st.calls;
+            const EngineIO eio = *const_cast<const EngineIO *>(&sh.eio);
+            sp[0] = eio.sweeps;
+            sp[1] = eio.passes;
+            sp[2] = eio.calls;
             sp[3] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.flips);
             sp[4] = st.cyc_prep;
-            sp[5] = st.cyc_jacobi;
-            sp[6] = st.cyc_update;
+            sp[5] = eio.cyc_jacobi;
+            sp[6] = eio.cyc_update;
             sp[7] = clock64() - t_img0;
-            sp[8] = st.cyc_tiny;
-            sp[9] = st.n_tiny;
-            sp[10] = st.pass_tiny;
-            sp[11] = st.cyc_dense;
-            sp[12] = st.n_dense;
-            sp[13] = st.pass_dense;
+            sp[8] = eio.cyc_tiny;
+            sp[9] = eio.n_tiny;
+            sp[10] = eio.pass_tiny;
+            sp[11] = eio.cyc_dense;
+            sp[12] = eio.n_dense;
+            sp[13] = eio.pass_dense;
             sp[14] = st.cyc_rank;
             sp[15] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.evals);
             for (int k = 0; k < 4; ++k) {
