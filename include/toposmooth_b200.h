@@ -153,8 +153,9 @@ int32_t ts_set_cta_threads(int32_t threads);
  * operations gate each image on its chunk and each chunk's copy-back on its
  * images); the results are unpacked on the host chunk by chunk; calls with
  * keep / avoid planes stream the uint8 planes (as 2); 2 = streamed uint8
- * chunks, no host packing; 0 = the chunked pipeline of separate launches.
- * Returns the previous value. */
+ * chunks, no host packing; 0 = the chunked pipeline of separate launches
+ * (always used under a serialising profiler -- ncu / nsys injection --
+ * or CUDA_LAUNCH_BLOCKING=1).  Returns the previous value. */
 int32_t ts_set_host_streaming(int32_t on);
 
 /* Tuning / A-B: 1 (default) = where eligible (one strip per thread, rows of

@@ -839,7 +839,16 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     const size_t img = (size_t)h * w, bytes = (size_t)n * img;
     const bool big = (long long)h * w > 1024LL * 1024;   // team-sized images: one chunk
     const MemOps &mo = memops();
-    if (!big && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR) {
+    // the streamed entry needs the copy engine to run while the kernel waits
+    // for it: not under a serialising profiler / injection library (ncu,
+    // nsys) or CUDA_LAUNCH_BLOCKING, where it would only time out
+    static const bool serialised = [] {
+        const char *lb = getenv("CUDA_LAUNCH_BLOCKING");
+        return getenv("CUDA_INJECTION64_PATH") != nullptr || getenv("NV_TPS_LAUNCH_TOKEN") != nullptr ||
+               getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr ||
+               getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr || (lb && lb[0] == '1');
+    }();
+    if (!big && !serialised && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR) {
         if (!keep_host && !avoid_host && g_streamed.load() == 1)
             return hasf_host_streamed_packed(in_host, out_host, n, h, w, r_max, fg, user, mo);
         return hasf_host_streamed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);
