@@ -83,7 +83,6 @@ struct Img {
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
     unsigned *bar;       // team barrier [count, generation] (G > 1)
-    unsigned *flags;     // 3 rotating "any change" flags (G > 1)
     int *err;
     struct Shared *sh;   // control block: shared memory (G == 1) or global (G > 1)
 };
@@ -125,18 +124,6 @@ __device__ __forceinline__ void team_sync(const Img &g) {
         __threadfence();
     }
     __syncthreads();
-}
-
-// team-wide OR of `v`; k = the team-uniform pass counter (rotating flags)
-__device__ __forceinline__ bool team_any(const Img &g, bool v, int k) {
-    if (g.G == 1) return __syncthreads_or(v);
-    const int any = __syncthreads_or(v);
-    if (threadIdx.x == 0) {
-        if (any) atomicOr(&g.flags[k % 3], 1u);
-        if (g.tid == 0) g.flags[(k + 1) % 3] = 0;   // next pass's flag (last read two barriers ago)
-    }
-    team_sync(g);
-    return *reinterpret_cast<volatile unsigned *>(&g.flags[k % 3]) != 0u;
 }
 
 struct Nb {
@@ -185,14 +172,6 @@ __device__ __forceinline__ void for_strip(const Img &g, F &&f) {
     walk_strips(g, [&](int x, int y0, int y1, int) {
         for (int y = y0; y < y1; ++y) f(y, x, pidx(g, y, x));
     });
-}
-
-// L1 prefetch through a generic address (a no-op for shared memory)
-#ifndef TS_PF
-#define TS_PF 1
-#endif
-__device__ __forceinline__ void prefetch_l1(const void *a) {
-    if (TS_PF) asm volatile("prefetch.L1 [%0];" ::"l"(a));
 }
 
 // ---- bit packing of uint8 {0,1} images ---------------------------------
@@ -467,10 +446,7 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
         for (int y = y0; y < y1; ++y, p += g.S) {
             Row3 rd[S];
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                rd[s] = row3(g.R + (size_t)s * g.plen, p + g.S);
-                prefetch_l1(g.R + (size_t)s * g.plen + p + 2 * g.S);   // next row (L2-resident slices)
-            }
+            for (int s = 0; s < S; ++s) rd[s] = row3(g.R + (size_t)s * g.plen, p + g.S);
             const Row3 id = row3(g.I, p + g.S);
             // E is read only for words holding candidates in some sweep of this
             // engine call, and those lie inside the unblocked target pixels
@@ -612,19 +588,12 @@ __device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, in
     add_count(cnt, counter);
 }
 
-// ---- fixpoint worklist: per-word pass stamps --------------------------------
-// Pass k (k = the team-uniform pass counter) re-evaluates the words stamped
-// k (by pass k - 1) or k + 1 (earlier in pass k) and stamps k + 1; stamps are
-// the counter's low byte (byte stores: all writers of a word store the same
-// value, so no atomics).  A stale stamp only costs an extra evaluation (any
+// ---- strip-walk pass stamps -------------------------------------------------
+// The strip-walk pass of a dense sweep (counter k) stamps the words it must
+// have re-evaluated with k + 1 (the counter's low byte; byte stores -- all
+// writers of a word store the same value, so no atomics); a scan then lists
+// them (collect_stamped).  A stale stamp only costs an extra evaluation (any
 // evaluation order reaches the same fixpoint).
-struct Marks {
-    uint8_t cur, next;
-};
-
-__device__ __forceinline__ Marks pass_marks(const Img &, int k) { return Marks{(uint8_t)k, (uint8_t)(k + 1)}; }
-
-__device__ __forceinline__ bool stamped(const Img &g, const Marks &m, int p) { return (uint8_t)(g.mark[p] - m.cur) <= 1; }
 
 // stamp, for re-evaluation in the next pass, the words whose inputs changed
 // when decision bits `chg` of word p flipped.  A pixel's decision reads the
@@ -751,9 +720,9 @@ __device__ __forceinline__ bool dense_pass(const Img &g, int pc, int &evals) {
 
 // variant for the L2-resident planes (generic / team kernel): measured faster there
 template <int FG>
-__device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, int pc, int &evals) {
+__device__ __forceinline__ bool dense_pass_l2(const Img &g, int pc, int &evals) {
     bool ch = false;
-    const Marks mk = pass_marks(g, pc);
+    const uint8_t next = (uint8_t)(pc + 1);
     auto strip = [&](int x, int y0, int y1, int) {
         if (y0 >= y1) return;
         int p = pidx(g, y0, x);
@@ -786,7 +755,7 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, int pc, i
                     const uint32_t chg = nd ^ dm.c;
                     g.D[p] = nd;
                     dm.c = nd;
-                    stamp_chg(g, p, chg, e0, e1, mk.next, true);
+                    stamp_chg(g, p, chg, e0, e1, next, true);
                     ch = true;
                 }
             }
@@ -799,7 +768,6 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, bool full, int pc, i
         };
         auto fetch = [&](int q, uint32_t &c, uint4 &e0, uint4 &e1) {
             c = g.C[q];
-            if (c && !(full || stamped(g, mk, q))) c = 0;
             if (c) {
                 const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
                 e0 = ep[0];
@@ -1020,7 +988,6 @@ struct Shared {
 struct TeamCtl {
     Shared sh;
     unsigned bar[2];
-    unsigned flags[3];
 };
 static_assert(sizeof(TeamCtl) <= kTeamCtlBytes, "kTeamCtlBytes too small");
 
@@ -1037,7 +1004,7 @@ struct View {
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank;
-    unsigned *bar, *flags;
+    unsigned *bar;
     int *err;
 };
 
@@ -1082,7 +1049,6 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.tid = HOT ? (int)threadIdx.x : v.rank * kThreads + (int)threadIdx.x;
     g.nthr = HOT ? kThreads : v.G * kThreads;
     g.bar = v.bar;
-    g.flags = v.flags;
     g.err = v.err;
     g.sh = g.G == 1 ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))
                     : reinterpret_cast<Shared *>(v.sh);
@@ -1557,7 +1523,7 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
     if (HOT)
         dense_pass<FG>(g, pc, o.evals);
     else
-        dense_pass_l2<FG>(g, true, pc, o.evals);
+        dense_pass_l2<FG>(g, pc, o.evals);
     ++o.passes;
     ++pc;
     team_sync(g);   // stamps of the strip-walk pass complete
@@ -1883,9 +1849,6 @@ __device__ __noinline__ void load_image_nl(const View &v, const KParams *pp, siz
     for (int q = tid; q < 2 * g.mw; q += nthr) g.claim[q] = 0;
     for (int q = tid; q < (g.plen + 15) >> 4; q += nthr)
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
-    if (g.G > 1 && tid == 0) {
-        g.flags[0] = g.flags[1] = g.flags[2] = 0;
-    }
     team_sync(g);
     if (p.packed_io) {   // host-packed bit rows (validated on the host)
         const uint32_t *src = reinterpret_cast<const uint32_t *>(p.in) + (size_t)img * g.H * g.WW;
@@ -1982,7 +1945,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     vl.G = G;
     vl.rank = rank;
     vl.bar = tc ? tc->bar : nullptr;
-    vl.flags = tc ? tc->flags : nullptr;
     vl.err = p.err;
     __shared__ View v_shared;
     if (threadIdx.x == 0) v_shared = vl;
