@@ -318,9 +318,11 @@ struct Lev {
 // xmode (thin) : 0 -> F = P > r^2 ; 1 -> | keep ; 2 -> | XS
 // xmode (thick): 0 -> V = D <= r^2 ; 1 -> & ~avoid ; 2 -> & XS
 // rank slices rs[] and blocked bits of word (y, x) (padded index p)
-template <int R>
-__device__ __forceinline__ uint32_t rank_word(const Img &g, int y, int x, int p, bool thin, int xmode,
+// THIN: -1 = runtime `thin`, 0 / 1 = compile-time (folds the seed inversion)
+template <int R, int THIN = -1>
+__device__ __forceinline__ uint32_t rank_word(const Img &g, int y, int x, int p, bool thin_rt, int xmode,
                                               uint32_t (&rs)[Lev<R>::S]) {
+    const bool thin = THIN < 0 ? thin_rt : THIN != 0;
     using LV = Lev<R>;
     constexpr int L = LV::L;
     constexpr int S = LV::S;
@@ -479,8 +481,10 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
 // own word row by row and keeps a 3-row window; the slices of the left / right
 // words (the neighbouring lanes, same row, same step) come by warp shuffles,
 // so the slices never touch memory and the two phases need no barrier between.
-template <int FG, int R>
-__device__ __forceinline__ void prep_fused(const Img &g, bool thin, int xmode, bool save_xs, int t, int *counter) {
+template <int FG, int R, bool THIN>
+__device__ __forceinline__ void prep_fused(const Img &g, int xmode, bool save_xs, int *counter) {
+    constexpr bool thin = THIN;
+    constexpr int t = THIN ? 1 : 0;
     constexpr int S = Lev<R>::S;
     const int lane = threadIdx.x & 31;
     const int x = g.tid % g.WW, blk = g.tid / g.WW;
@@ -497,7 +501,7 @@ __device__ __forceinline__ void prep_fused(const Img &g, bool thin, int xmode, b
         if (in) {
             const int p = pidx(g, y, x);
             const uint32_t xs = g.I[p];
-            bl = rank_word<R>(g, y, x, p, thin, xmode, rs);
+            bl = rank_word<R, THIN ? 1 : 0>(g, y, x, p, thin, xmode, rs);
             if (y >= y0 && y < y1) {
                 g.B[p] = bl;
                 if (save_xs) g.XS[p] = xs;
@@ -1100,7 +1104,11 @@ static_assert(kMaxSlices <= 7, "epass_dispatch covers up to 7 rank slices");
 template <int FG, bool HOT, int R>
 __device__ __noinline__ void prep_fused_nl(const View &v, bool thin, int xmode, bool save_xs, int t, int cur) {
     const Img g = make_img<HOT>(v);
-    prep_fused<FG, R>(g, thin, xmode, save_xs, t, &g.sh->counters[cur]);
+    (void)t;   // == thin
+    if (thin)
+        prep_fused<FG, R, true>(g, xmode, save_xs, &g.sh->counters[cur]);
+    else
+        prep_fused<FG, R, false>(g, xmode, save_xs, &g.sh->counters[cur]);
 }
 
 // fused prep + E-pass (see prep_fused); false when not eligible
