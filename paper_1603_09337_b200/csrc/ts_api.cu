@@ -278,7 +278,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     pl.smem_bytes = (size_t)(used * 4);
     pl.stride_ws = gused;
     const uint32_t hot_mask =
-        (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_DIRTY) | (1u << B_MARK) | (1u << B_CLAIM);
+        (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_DIRTY) | (1u << B_MARK) | (1u << B_CLAIM) | (1u << B_B);
     pl.hot = (pl.mask & hot_mask) == hot_mask;
     if (fused && !pl.hot)   // the fused path runs only with the hot placement: plan the R planes
         return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, budget_cap, true);

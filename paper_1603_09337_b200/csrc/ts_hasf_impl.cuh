@@ -1002,8 +1002,8 @@ static_assert(sizeof(TeamCtl) <= kTeamCtlBytes, "kTeamCtlBytes too small");
 // cvta inside the callee (so accesses compile to LDS/STS), others as pointers.
 struct View {
     unsigned long long I, D, C, dirty, mark;   // shared address (HOT) or pointer bits
-    uint32_t *B, *list, *E, *XS, *R, *K, *A;
-    unsigned long long claim;   // shared address (HOT) or pointer bits
+    uint32_t *list, *E, *XS, *R, *K, *A;
+    unsigned long long B, claim;   // shared address (HOT) or pointer bits
     int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, fused, mw;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
@@ -1028,7 +1028,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.C = hot_ptr<HOT>(v.C);
     g.dirty = hot_ptr<HOT>(v.dirty);
     g.mark = reinterpret_cast<uint8_t *>(hot_ptr<HOT>(v.mark));
-    g.B = v.B;
+    g.B = hot_ptr<HOT>(v.B);
     g.claim = hot_ptr<HOT>(v.claim);
     g.mw = v.mw;
     g.list = v.list;
@@ -1927,7 +1927,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         vl.dirty = (unsigned long long)buf(B_DIRTY);
         vl.mark = (unsigned long long)buf(B_MARK);
     }
-    vl.B = buf(B_B);
+    vl.B = HOT ? (unsigned long long)__cvta_generic_to_shared(smem) + 4ull * p.off[B_B]
+               : (unsigned long long)buf(B_B);
     vl.claim = HOT ? (unsigned long long)__cvta_generic_to_shared(smem) + 4ull * p.off[B_CLAIM]
                    : (unsigned long long)buf(B_CLAIM);
     vl.mw = p.mwords;

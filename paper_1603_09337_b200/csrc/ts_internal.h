@@ -99,7 +99,7 @@ struct KParams {
     uint32_t *gws;          // global workspace, gws_stride words per CTA
     long long gws_stride;
     uint32_t smem_mask;     // bit b set: buffer b lives in shared memory
-    int hot;                // I, D, C, B, DIRTY, MARK all in shared memory (fast variant)
+    int hot;                // I, D, C, B, DIRTY, MARK, CLAIM all in shared memory (fast variant)
     long long off[B_COUNT]; // word offset of each buffer (smem or CTA slice)
     int *counter;           // image queue head
     // streamed host entry (or null): image i waits for ready[i / chunk] != 0
