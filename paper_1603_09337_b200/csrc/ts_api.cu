@@ -567,6 +567,16 @@ const MemOps &memops() {
 }
 std::atomic<int> g_streamed{1};
 
+// uint8 bytes per streamed chunk (TS_CHUNK_BYTES overrides, for measurements)
+size_t chunk_bytes() {
+    static const size_t b = [] {
+        const char *e = getenv("TS_CHUNK_BYTES");
+        const long long v = e ? atoll(e) : 0;
+        return v > 0 ? (size_t)v : (size_t)(4u << 20);
+    }();
+    return b;
+}
+
 // chunk flag buffers for the streamed entry: plain cudaMalloc allocations
 // (stream memory operations target them), recycled, never freed
 constexpr int kMaxChunks = 64;
@@ -597,7 +607,7 @@ int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
                        const MemOps &mo) {
     const size_t img = (size_t)h * w, bytes = (size_t)n * img;
     // chunks of ~4 MB (16 images at 512^2), at most 64 of them
-    int64_t chunk = std::max<int64_t>(1, (int64_t)((4u << 20) / std::max<size_t>(img, 1)));
+    int64_t chunk = std::max<int64_t>(1, (int64_t)(chunk_bytes() / std::max<size_t>(img, 1)));
     chunk = std::max<int64_t>(chunk, (n + kMaxChunks - 1) / kMaxChunks);
     const int nchunks = (int)((n + chunk - 1) / chunk);
     const int nbuf = 2 + (keep_host ? 1 : 0) + (avoid_host ? 1 : 0);
@@ -728,7 +738,7 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
                               int32_t r_max, int32_t fg, cudaStream_t user, const MemOps &mo) {
     const int ww = (w + 31) / 32;
     const size_t img = (size_t)h * w, wimg = (size_t)h * ww, words = (size_t)n * wimg;
-    int64_t chunk = std::max<int64_t>(1, (int64_t)((4u << 20) / std::max<size_t>(img, 1)));
+    int64_t chunk = std::max<int64_t>(1, (int64_t)(chunk_bytes() / std::max<size_t>(img, 1)));
     chunk = std::max<int64_t>(chunk, (n + kMaxChunks - 1) / kMaxChunks);
     const int nchunks = (int)((n + chunk - 1) / chunk);
     std::lock_guard<std::mutex> lk(g_stage_mu);
