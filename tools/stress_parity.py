@@ -34,15 +34,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=300)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--max-size", type=int, default=300, help="largest side (exclusive)")
+    ap.add_argument("--max-r", type=int, default=8)
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     lib = _lib.load()
     bad = 0
     for i in range(a.cases):
-        h, w = int(rng.integers(1, 300)), int(rng.integers(1, 300))
-        n = int(rng.integers(1, 6))
+        h, w = int(rng.integers(1, a.max_size)), int(rng.integers(1, a.max_size))
+        n = int(rng.integers(1, 6 if a.max_size <= 300 else 3))
         fg = int(rng.choice([4, 8]))
-        r = int(rng.integers(0, 9))
+        r = int(rng.integers(0, a.max_r + 1))
         imgs = np.stack([rand_img(rng, h, w) for _ in range(n)])
         keep = avoid = None
         if rng.random() < 0.3:
