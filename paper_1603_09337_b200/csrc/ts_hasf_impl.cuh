@@ -26,26 +26,32 @@
 // flips iff SIMPLE(code of p with every candidate neighbour q that precedes p
 // in key order toggled iff q flips).  The precedence masks ("E" planes) are
 // computed once per engine call from the rank slices.  Any evaluation order
-// reaches the unique solution; a pass in which no decision changes certifies
-// it.  Two sweep modes:
-//   dense  (many candidates): every thread walks its vertical strip of words
-//          with a sliding 3-row register window (updates propagate down the
-//          strip within a pass), candidates kept in the C plane;
-//   sparse (few candidates): an active-word list, the thread's first word's
-//          sweep-constant data cached in registers, one warp only when <= 32
-//          words; the next sweep re-examines only the 3x3 word neighbourhoods
-//          of the flips (the reference's re-queue, topo.py:245-257) found
-//          through a 1-bit-per-word dirty bitmap.
-// After the first pass of a sweep only words stamped by a changed neighbour
-// decision are re-evaluated (a worklist of per-word pass stamps).
+// reaches the unique solution.  A pixel reads only the decisions of the
+// neighbours that precede it, so when a word's decisions change only the
+// neighbour words named by its own E masks can be affected: those are
+// re-evaluated, and a pass that affects no candidate word certifies the
+// fixpoint.  Sweep modes:
+//   dense  (many candidates): one strip-walk pass -- every thread walks its
+//          vertical strip of words with a sliding 3-row register window
+//          (updates propagate down the strip), byte-stamping the affected
+//          words; a scan lists them; then claim passes: one listed word per
+//          thread, changed words claim their affected candidate words into
+//          the next pass's list (claim bitmap: first claimant appends);
+//   list   (fewer candidates): claim passes from the sweep's word list, then
+//          the 3x3 word neighbourhoods of the flips (the reference's
+//          re-queue, topo.py:245-257) are re-examined through a dirty bitmap
+//          compacted into a word list;
+//   tiny   (<= 32 words): warp 0 runs whole sweeps alone, warp syncs only.
 //
 // Layout: every plane is padded with one zero row above and below and
 // one zero word between rows (row stride S >= WW + 1, chosen on the host so
 // the 32 lanes of a warp touch 32 distinct banks), so neighbour and disc
-// accesses need no bounds checks.  The hot planes (I, D, C, B, the dirty
-// bitmap and the stamps) live in shared memory when they fit (HOT variant,
-// accessed as LDS/STS); E, rank slices, saved image, list spill to the CTA's
-// slice of an L2-resident global workspace when shared memory runs out.
+// accesses need no bounds checks.  The hot planes (I, D, C, B, the dirty /
+// claim bitmaps and the stamps) live in shared memory when they fit (HOT
+// variant, accessed as LDS/STS); lists, saved image, E and rank slices follow
+// in shared memory while they fit, the rest in the CTA's slice of an
+// L2-resident global workspace.  The phase functions take the per-CTA View by
+// reference from shared memory (a by-value View cost 15% in ABI copies).
 #pragma once
 #include <cuda_runtime.h>
 #include "ts_common.cuh"
