@@ -79,13 +79,20 @@ __global__ void ccl_union(CclArgs a) {
         int *parent = a.parent + b * per;
         const int r = (int)(q / a.w), c = (int)(q - (size_t)r * a.w);
         const int p = (int)q;
-        if (c > 0 && img[q - 1] == a.target) unite(parent, p, p - 1);
-        if (r > 0) {
-            if (img[q - a.w] == a.target) unite(parent, p, p - a.w);
-            if (a.conn == 8) {
-                if (c > 0 && img[q - a.w - 1] == a.target) unite(parent, p, p - a.w - 1);
-                if (c + 1 < a.w && img[q - a.w + 1] == a.target) unite(parent, p, p - a.w + 1);
-            }
+        const bool W = c > 0 && img[q - 1] == a.target;
+        const bool N = r > 0 && img[q - a.w] == a.target;
+        if (W) unite(parent, p, p - 1);
+        if (a.conn == 8) {
+            // edges implied by others are skipped (8-adjacency): W-N, NW-W, NW-N
+            // and N-NE are themselves neighbour pairs, so one union per
+            // connected group of earlier neighbours suffices
+            const bool NW = r > 0 && c > 0 && img[q - a.w - 1] == a.target;
+            const bool NE = r > 0 && c + 1 < a.w && img[q - a.w + 1] == a.target;
+            if (N && !W) unite(parent, p, p - a.w);
+            if (NW && !W && !N) unite(parent, p, p - a.w - 1);
+            if (NE && !N) unite(parent, p, p - a.w + 1);
+        } else if (N) {
+            unite(parent, p, p - a.w);
         }
         // pixels on the window border touch the exterior ring (the ring pixels
         // are 4- and 8-adjacent to every border pixel)
@@ -102,7 +109,12 @@ __global__ void ccl_count(CclArgs a) {
         const bool ext = q == hw;
         // roots only: when border pixels attached the exterior node it hangs under
         // the smallest pixel index of that component
-        if (v == (int)q && (!ext || a.exterior)) atomicAdd((unsigned long long *)&a.counts[b], 1ull);
+        const bool root = v == (int)q && (!ext || a.exterior);
+        // one atomic per image run of the warp (lanes of a warp mostly share b)
+        const unsigned act = __activemask();
+        const unsigned same = __match_any_sync(act, (unsigned long long)b);
+        const unsigned cnt = __popc(__ballot_sync(act, root) & same);
+        if (cnt && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd((unsigned long long *)&a.counts[b], (unsigned long long)cnt);
     }
 }
 
