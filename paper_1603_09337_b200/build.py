@@ -37,7 +37,20 @@ def needs_build() -> bool:
 
 def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
     """Compile all translation units in parallel and link the shared library.
-    `defines` (e.g. ["TS_MIN_BLOCKS=1"]) and `out` build experiment variants."""
+    `defines` (e.g. ["TS_MIN_BLOCKS=1"]) and `out` build experiment variants.
+    Serialised across processes by an flock (torchrun ranks importing a stale
+    tree build once; the others wait and then find it current)."""
+    import fcntl
+    os.makedirs(OBJ, exist_ok=True)
+    with open(os.path.join(OBJ, ".build.lock"), "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        try:
+            return _build_locked(verbose, force, defines, out)
+        finally:
+            fcntl.flock(lock, fcntl.LOCK_UN)
+
+
+def _build_locked(verbose, force, defines, out):
     lib = out or LIB
     if not force and not defines and out is None and not needs_build():
         return LIB
@@ -63,7 +76,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
         objs.append(obj)
     if failed:
         raise RuntimeError(f"nvcc failed on {failed}")
-    tmp = lib + ".tmp"
+    tmp = f"{lib}.tmp{os.getpid()}"   # per-process: ranks never share a temp file
     res = subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lgomp"], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

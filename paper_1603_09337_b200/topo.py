@@ -24,7 +24,45 @@ from .grid import ADJ_84, Adjacency, as_binary
 _OFFSETS = ((-1, -1), (-1, 0), (-1, 1), (0, -1), (0, 1), (1, -1), (1, 0), (1, 1))   # topo.py:35
 
 
+def _comp_count(mask: int, conn: int) -> int:
+    """Components of the set neighbours of a 3x3 window's centre (conn-adjacent
+    to each other) that touch the centre under conn (topo.py:44-76)."""
+    parent = list(range(8))
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+
+    for a in range(8):
+        for b in range(a + 1, 8):
+            if not ((mask >> a) & 1 and (mask >> b) & 1):
+                continue
+            dr = abs(_OFFSETS[a][0] - _OFFSETS[b][0])
+            dc = abs(_OFFSETS[a][1] - _OFFSETS[b][1])
+            if (dr + dc == 1) if conn == 4 else (dr <= 1 and dc <= 1):
+                parent[find(a)] = find(b)
+    roots = {find(a) for a in range(8)
+             if (mask >> a) & 1 and (conn == 8 or _OFFSETS[a][0] == 0 or _OFFSETS[a][1] == 0)}
+    return len(roots)
+
+
 def _tables():
+    """T8/T4 and the simple-point LUTs (topo.py:79-84), built at import on the
+    host -- no native library load, so importing the package (e.g. for its
+    workload generators) never maps libtoposmooth_b200.so.  The library holds
+    the same tables (ts_connectivity_tables; tests check they agree)."""
+    t8 = np.array([_comp_count(m, 8) for m in range(256)], np.uint8)
+    t4 = np.array([_comp_count(m, 4) for m in range(256)], np.uint8)
+    inv = np.arange(256) ^ 0xFF
+    s84 = ((t8 == 1) & (t4[inv] == 1)).astype(np.uint8)
+    s48 = ((t4 == 1) & (t8[inv] == 1)).astype(np.uint8)
+    return t8, t4, s84, s48
+
+
+def native_tables():
+    """The library's copy of the four tables (ts_connectivity_tables)."""
     bufs = [(ctypes.c_uint8 * 256)() for _ in range(4)]
     check(load().ts_connectivity_tables(*[ctypes.addressof(b) for b in bufs]))
     return [np.frombuffer(b, dtype=np.uint8).copy() for b in bufs]
