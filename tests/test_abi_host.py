@@ -169,3 +169,18 @@ def test_device_calls_fail_loudly_without_gpu():
         P.smooth(np.zeros((4, 4), np.uint8), 1)
     with pytest.raises(RuntimeError, match="CUDA"):
         P.edt_squared(np.zeros((4, 4), np.uint8))
+
+
+def test_package_import_maps_no_native_library():
+    """Importing the package (e.g. for its generators, as bench.py's reference
+    arm does) must not map libtoposmooth_b200.so; the host-side tables equal
+    the library's."""
+    import subprocess
+    import sys
+    code = ("import paper_1603_09337_b200 as P\n"
+            "print(any('libtoposmooth' in l for l in open('/proc/self/maps')))\n")
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=REPO, timeout=300)
+    assert res.stdout.strip().splitlines()[-1] == "False", res.stderr
+    from paper_1603_09337_b200 import topo
+    for a, b in zip(topo.native_tables(), (topo.T8_TABLE, topo.T4_TABLE, topo.SIMPLE_84, topo.SIMPLE_48)):
+        assert np.array_equal(a, b)

@@ -1,6 +1,8 @@
 """Parity of the CUDA path (through the C ABI) against the reference's golden
 vectors and the CPU oracle.  Bit-exact everywhere (all arithmetic is integer)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -8,7 +10,7 @@ import oracle as O
 import paper_1603_09337_b200 as P
 from paper_1603_09337_b200 import _lib
 from paper_1603_09337_b200 import workloads as W
-from conftest import golden_cases, random_image
+from conftest import GOLDEN, golden_cases, random_image
 
 pytestmark = pytest.mark.gpu
 
@@ -376,3 +378,39 @@ def test_streamed_host_entry_vs_device_path(streaming):
         assert rc == _lib.TS_ERR_VALUE and b"0 or 1" in lib.ts_last_error()
     finally:
         lib.ts_set_host_streaming(old)
+
+
+# ---- large configs pinned to the reference (tests/golden/make_golden_large.py) ----
+def _sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, np.uint8).tobytes()).hexdigest()
+
+
+def _first_mismatch(got, bits):
+    want = np.unpackbits(bits)[: got.size].reshape(got.shape)
+    ys, xs = np.nonzero(got != want)
+    return f"{len(ys)} pixels differ, first at ({ys[0]}, {xs[0]})" if len(ys) else "equal"
+
+
+def test_c3_full_size_bit_exact():
+    """Config c3 (8192^2, r = 1..8, (8,4)): the whole image bit-exact against
+    the reference's own hasf output (SHA-256 + packed bits, generated by
+    importing /root/reference, smoothing.py:187-212)."""
+    z = np.load(os.path.join(GOLDEN, "large.npz"))
+    cfg = W.CONFIGS["c3"]
+    img = W.config_image(cfg, 0)
+    assert _sha(img) == str(z["c3_0_in_sha"]), "generator drift: c3 input differs from the pinned one"
+    out = P.hasf_batch(img[None], cfg.r_max)[0]
+    assert _sha(out) == str(z["c3_0_out_sha"]), _first_mismatch(out, z["c3_0_out_bits"])
+
+
+def test_c2_full_batch_bit_exact():
+    """Config c2 as bench.py runs it: the full 32-image 2048^2 batch in one
+    launch (team layout), four images pinned to the reference's hasf."""
+    z = np.load(os.path.join(GOLDEN, "large.npz"))
+    cfg = W.CONFIGS["c2"]
+    imgs = W.config_batch(cfg, 0, cfg.n)
+    out = P.hasf_batch(torch.from_numpy(imgs).cuda(), cfg.r_max).cpu().numpy()
+    for i in (1, 7, 19, 31):
+        assert _sha(imgs[i]) == str(z[f"c2_{i}_in_sha"]), f"generator drift on c2[{i}]"
+        assert _sha(out[i]) == str(z[f"c2_{i}_out_sha"]), f"c2[{i}]: " + _first_mismatch(out[i], z[f"c2_{i}_out_bits"])

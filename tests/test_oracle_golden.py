@@ -86,3 +86,20 @@ def test_hasf_batch_threads_match_serial():
     out = O.hasf_batch(imgs, 4, 4, threads=4)
     for k, c in enumerate(z):
         assert np.array_equal(out[k], c["out"]), c["name"]
+
+
+def test_large_goldens_inputs_and_oracle_c2():
+    """tests/golden/large.npz (reference hasf on c2 / c3 config images): the
+    generators still reproduce the pinned inputs, and the oracle matches the
+    reference on one full-size c2 image (2048^2, r = 1..10)."""
+    import hashlib
+    import os
+    from conftest import GOLDEN
+    from paper_1603_09337_b200 import workloads as W
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a, np.uint8).tobytes()).hexdigest()  # noqa: E731
+    z = np.load(os.path.join(GOLDEN, "large.npz"))
+    cfg = W.CONFIGS["c2"]
+    for i in (1, 7, 19, 31):
+        assert sha(W.config_image(cfg, i)) == str(z[f"c2_{i}_in_sha"])
+    img = W.config_image(cfg, 31)
+    assert sha(O.hasf(img, cfg.r_max, 8)) == str(z["c2_31_out_sha"])
