@@ -164,6 +164,33 @@ int32_t ts_set_host_streaming(int32_t on);
  * through the rank planes.  Returns the previous value. */
 int32_t ts_set_fused_prep(int32_t on);
 
+/* Tuning / A-B of the segmented scheduler: batches with more single-CTA
+ * images than one wave of CTAs are handed out as (segment, image) tasks of
+ * `stages` consecutive stages (4 stages = one radius: S1/S3 cutting, S5/S7
+ * filling, each a prep + engine call), segment-major, so the SMs left idle
+ * when the queue drains wait for at most one segment instead of one whole
+ * image.  The image's bit-plane passes between segments through global
+ * memory; results are identical.  0 = whole images; default 4 (one radius;
+ * env TS_SEG_STAGES overrides at load).  Returns the previous value. */
+int32_t ts_set_segment_stages(int32_t stages);
+
+/* Tuning / A-B: the last `stages` stages of an image run as one-stage
+ * segments (the queue's drain then waits for at most one short stage);
+ * default 2 (env TS_SEG_FINE).  Returns the previous value. */
+int32_t ts_set_segment_fine(int32_t stages);
+
+/* Testing: 1 = segment batches of any size (tasks then often wait for their
+ * predecessor segment on another SM).  Returns the previous value. */
+int32_t ts_set_segment_force(int32_t on);
+
+/* Debug: record, for the first `tasks` tasks of every later fused launch, 7
+ * int64 per task into the device buffer trace_dev: SM id, then %globaltimer
+ * (ns) when the task was taken from the queue, when its input was ready (after
+ * any wait for the predecessor segment / input chunk), loaded into the CTA,
+ * its stages were done, its result stored, and the task finished.  Task t =
+ * segment * n + image (segmented) or image.  NULL disables. */
+void ts_set_trace(int64_t *trace_dev, int64_t tasks);
+
 /* Placement/occupancy the fused kernel would use for an image shape:
  * info[0] = grid CTAs per wave, info[1] = CTAs per SM, info[2] = smem bytes,
  * info[3] = smem buffer mask, info[4] = global workspace bytes per CTA,

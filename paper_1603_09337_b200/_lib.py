@@ -49,6 +49,10 @@ SIGNATURES = {
     "ts_set_cta_threads": ([_i32], _i32),
     "ts_set_host_streaming": ([_i32], _i32),
     "ts_set_fused_prep": ([_i32], _i32),
+    "ts_set_segment_stages": ([_i32], _i32),
+    "ts_set_segment_fine": ([_i32], _i32),
+    "ts_set_segment_force": ([_i32], _i32),
+    "ts_set_trace": ([_vp, _i64], None),
     "ts_hasf_plan": ([_i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int),
 }
 
@@ -67,6 +71,8 @@ def load(build_if_missing: bool = True):
             raise RuntimeError(f"CUDA library missing: {LIB_PATH} (run python -m paper_1603_09337_b200.build)")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (argt, rest) in SIGNATURES.items():
+            if os.environ.get("TS_LIB_PATH") and not hasattr(lib, name):
+                continue   # A/B against an older experimental build
             fn = getattr(lib, name)
             fn.argtypes = argt
             fn.restype = rest

@@ -127,6 +127,20 @@ struct Plan {
 };
 
 std::atomic<int> g_fused{1};      // fused prep + E-pass where eligible
+std::atomic<long long *> g_trace_buf{nullptr};   // debug task trace (ts_set_trace)
+std::atomic<long long> g_trace_cap{0};
+// stages per segment of the segmented scheduler (0: whole images); 2 = half a
+// radius (one cutting or one filling), the image state between them is one plane
+std::atomic<int> g_seg_stages{[] {
+    const char *e = getenv("TS_SEG_STAGES");
+    return e ? atoi(e) : 4;
+}()};
+std::atomic<int> g_seg_force{0};   // tests: segment batches of any size
+// the last g_seg_fine stages run as one-stage segments (env TS_SEG_FINE)
+std::atomic<int> g_seg_fine{[] {
+    const char *e = getenv("TS_SEG_FINE");
+    return e ? atoi(e) : 2;
+}()};
 std::atomic<int> g_dense_div{4};   // measured: 4 beats 2 by ~1.5% on c1, neutral on c4
 
 // strip mapping (thread t -> word column t % WW, row block t / WW) and the
@@ -387,15 +401,30 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     }
     const int teams = (int)std::min<long long>(n, pl.per_wave / team);
     const int grid = teams * team;
+    // segmented scheduling: a batch larger than one wave of single-CTA images
+    // is handed out as (segment, image) tasks, so the last wave's idle SMs are
+    // bounded by one segment instead of one whole image (KParams::nseg)
+    const int nst = (do_cut ? 2 : 0) + (do_fill ? 2 : 0);
+    const int total_stages = mode == MODE_HASF ? (r_last - r_first + 1) * nst : 0;
+    // segments of seg_stages stages, the last `fine` stages one per segment
+    // (the tail when the queue drains is then at most one short stage)
+    const int seg_stages = g_seg_stages.load(), fine = std::max(0, g_seg_fine.load());
+    int nseg = 1;
+    if (mode == MODE_HASF && team == 1 && seg_stages > 0 && (n > pl.per_wave || g_seg_force.load()) &&
+        total_stages > 1)
+        nseg = seg_count(total_stages, seg_stages, fine);
     const size_t ws_words = (size_t)pl.stride_ws * (team > 1 ? teams : grid);
+    const size_t xbuf_words = nseg > 1 ? (size_t)n * 2 * h * pl.WW : 0;
     const size_t tctl_bytes = team > 1 ? (size_t)teams * kTeamCtlBytes : 0;
-    const size_t ctrl_bytes = 64 + (stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0) + tctl_bytes;
+    const size_t stats_bytes = stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0;
+    const size_t prog_bytes = nseg > 1 ? (((size_t)n * sizeof(unsigned) + 63) & ~(size_t)63) : 0;
+    const size_t ctrl_bytes = 64 + stats_bytes + prog_bytes + tctl_bytes;
     if (team_out) *team_out = team;
     char *ctrl = nullptr;
     uint32_t *gws = nullptr;
     TS_CUDA(cudaMallocAsync((void **)&ctrl, ctrl_bytes, st));
-    if (ws_words) {
-        cudaError_t e = cudaMallocAsync((void **)&gws, ws_words * 4, st);
+    if (ws_words + xbuf_words) {
+        cudaError_t e = cudaMallocAsync((void **)&gws, (ws_words + xbuf_words) * 4, st);
         if (e != cudaSuccess) {
             cudaFreeAsync(ctrl, st);
             return cuda_fail(e, "cudaMallocAsync(workspace)");
@@ -444,6 +473,13 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.ready = ready;
     p.done = done;
     p.chunk = chunk;
+    p.trace = g_trace_buf.load();
+    p.trace_cap = g_trace_cap.load();
+    p.nseg = nseg;
+    p.seg_stages = seg_stages;
+    p.seg_fine = fine;
+    p.xbuf = nseg > 1 ? gws + ws_words : nullptr;
+    p.progress = nseg > 1 ? reinterpret_cast<unsigned *>(ctrl + 64 + stats_bytes) : nullptr;
     cudaError_t le = launch_hasf(p, fg, grid, pl.smem_bytes, st);
     cudaError_t ce = cudaSuccess;
     if (le == cudaSuccess && stats_host)
@@ -833,6 +869,17 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
 int32_t ts_set_host_streaming(int32_t on) { return g_streamed.exchange(on < 0 ? 0 : (on > 2 ? 2 : on)); }
 
 int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
+
+int32_t ts_set_segment_stages(int32_t stages) { return g_seg_stages.exchange(stages < 0 ? 0 : stages); }
+
+int32_t ts_set_segment_fine(int32_t stages) { return g_seg_fine.exchange(stages < 0 ? 0 : stages); }
+
+int32_t ts_set_segment_force(int32_t on) { return g_seg_force.exchange(on ? 1 : 0); }
+
+void ts_set_trace(int64_t *trace_dev, int64_t tasks) {
+    g_trace_cap.store(trace_dev ? tasks : 0);
+    g_trace_buf.store(reinterpret_cast<long long *>(trace_dev));
+}
 
 int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w, int32_t r_max,
                        int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host, void *stream) {

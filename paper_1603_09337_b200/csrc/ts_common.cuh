@@ -96,4 +96,22 @@ __device__ __forceinline__ uint32_t simple_bits(uint32_t nw, uint32_t n, uint32_
     return (x1 ^ x2) & ~(c1 | c2);    // exactly one of t1,t3,t5,t7
 }
 
+// segmented scheduler (KParams::nseg): segment `seg` of an image's `total`
+// stages is [k0, k1): segments of `len` stages, the last `fine` stages one each
+__host__ __device__ __forceinline__ int seg_count(int total, int len, int fine) {
+    const int body = total > fine ? total - fine : 0;
+    return (body + len - 1) / len + (total - body);
+}
+__host__ __device__ __forceinline__ void seg_range(int total, int len, int fine, int seg, int &k0, int &k1) {
+    const int body = total > fine ? total - fine : 0;
+    const int nbody = (body + len - 1) / len;
+    if (seg < nbody) {
+        k0 = seg * len;
+        k1 = k0 + len < body ? k0 + len : body;
+    } else {
+        k0 = body + (seg - nbody);
+        k1 = k0 + 1;
+    }
+}
+
 }  // namespace ts

@@ -1894,6 +1894,65 @@ __device__ __noinline__ void load_image_nl(const View &v, const KParams *pp, siz
     });
 }
 
+// segment prologue (segmented scheduling, see KParams::nseg): the image's
+// bit-plane from xbuf (written by the predecessor segment, possibly on another
+// SM: L2 loads, never a stale L1 line), the constraint planes re-packed.  The
+// other planes carry no image state between stages (each prep rewrites B, C, D,
+// XS, E; the bitmaps are zero between engine calls); `clear` initialises them
+// (pads included) when this CTA has not run an image yet.
+template <bool HOT>
+__device__ __noinline__ void load_state_nl(const View &v, const KParams *pp, size_t pix, int img, bool clear,
+                                           bool with_xs) {
+    const KParams &p = *pp;
+    const Img g = make_img<HOT>(v);
+    const int tid = g.tid, nthr = g.nthr;
+    if (clear) {
+        for (int q = tid; q < g.plen; q += nthr) {
+            g.I[q] = 0;
+            g.D[q] = 0;
+            g.C[q] = 0;
+            g.B[q] = ~0u;
+        }
+        for (int q = tid; q < (g.plen + 31) >> 5; q += nthr) g.dirty[q] = 0;
+        for (int q = tid; q < 2 * g.mw; q += nthr) g.claim[q] = 0;
+    }
+    for (int q = tid; q < (g.plen + 15) >> 4; q += nthr)
+        reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
+    if (clear) team_sync(g);
+    const size_t wimg = (size_t)g.H * g.WW;
+    const uint32_t *src = p.xbuf + (size_t)img * 2 * wimg;
+    // the strip's words are requested together (L2 latency paid once per batch)
+    auto copy_in = [&](const uint32_t *from, uint32_t *to) {
+        walk_strips(g, [&](int x, int y0, int y1, int) {
+            constexpr int kB = 16;
+            for (int yb = y0; yb < y1; yb += kB) {
+                uint32_t w[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+                    if (yb + j < y1) w[j] = __ldcg(from + (size_t)(yb + j) * g.WW + x);
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+                    if (yb + j < y1) to[pidx(g, yb + j, x)] = w[j];
+            }
+        });
+    };
+    copy_in(src, g.I);
+    if (with_xs) copy_in(src + wimg, g.XS);
+    if (p.keep) pack_plane(p.keep + pix, g.K, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+    if (p.avoid) pack_plane(p.avoid + pix, g.A, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+}
+
+// segment epilogue: the bit-plane to xbuf for the next segment (L2)
+template <bool HOT>
+__device__ __noinline__ void store_state_nl(const View &v, uint32_t *dst, bool with_xs) {
+    const Img g = make_img<HOT>(v);
+    const size_t wimg = (size_t)g.H * g.WW;
+    for_strip(g, [&](int y, int x, int q) {
+        __stcg(dst + (size_t)y * g.WW + x, g.I[q]);
+        if (with_xs) __stcg(dst + wimg + (size_t)y * g.WW + x, g.XS[q]);
+    });
+}
+
 template <bool HOT>
 __device__ __noinline__ void store_image_nl(const View &v, uint8_t *out, uint32_t *out_bits) {
     const Img g = make_img<HOT>(v);
@@ -1902,6 +1961,9 @@ __device__ __noinline__ void store_image_nl(const View &v, uint8_t *out, uint32_
     else
         unpack_plane(g.I, out, g);
 }
+
+// stages S3 / S7 (stg 1 / 3) read the plane XS saved by the stage before them
+__device__ __forceinline__ bool reads_xs(int stg) { return stg == 1 || stg == 3; }
 
 // HOT: one CTA per image, hot planes in shared memory.  !HOT: a team of
 // p.team CTAs per image (consecutive blockIdx), planes in the team's slice of
@@ -1970,12 +2032,39 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     const bool has_k = p.keep != nullptr, has_a = p.avoid != nullptr;
     const bool lead = gk.tid == 0;
 
+    // stage list of one image: k = (r - r_first) * nst + (stg - first)
+    const int first = p.do_cut ? 0 : 2, last = p.do_fill ? 3 : 1;
+    const int nst = last - first + 1;
+    const int total_stages = p.mode == MODE_HASF ? (p.r_last - p.r_first + 1) * nst : 0;
+    const int nseg = p.nseg;
+    bool inited = false;   // this CTA's planes initialised (pads) by a first image load
     for (;;) {
         if (lead) sh.img = atomicAdd(p.counter, 1);
         team_sync(gk);
-        const int img = *reinterpret_cast<volatile int *>(&sh.img);
-        if (img >= p.n) break;
-        if (p.ready) {   // streamed host entry: wait for the image's input chunk
+        const int task = *reinterpret_cast<volatile int *>(&sh.img);
+        if (task >= p.n * nseg) break;
+        const int seg = task / p.n, img = task - seg * p.n;
+        unsigned long long tr0 = 0;
+        if (p.trace && lead) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+        int k0 = 0, k1 = total_stages;
+        if (nseg > 1) seg_range(total_stages, p.seg_stages, p.seg_fine, seg, k0, k1);
+        if (seg > 0) {   // segmented: wait until the predecessor segment published the image
+            if (lead) {
+                const unsigned *f = p.progress + img;
+                long long spins = 0;
+                unsigned v;
+                while (true) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    if ((int)v >= seg) break;
+                    __nanosleep(128);
+                    if (++spins > (1LL << 25)) {   // seconds: the predecessor was lost
+                        set_err(p.err, ERR_TEAM_TIMEOUT);
+                        break;
+                    }
+                }
+            }
+            team_sync(gk);
+        } else if (p.ready) {   // streamed host entry: wait for the image's input chunk
             if (lead) {
                 const unsigned *f = p.ready + img / p.chunk;
                 long long spins = 0;
@@ -2005,8 +2094,28 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.ystat[0] = sh.ystat[1] = sh.ystat[2] = sh.ystat[3] = 0;
             sh.eio = EngineIO{};
         }
-        load_image_nl<HOT>(v, &p, pix, img);
+        // debug trace: [smid, grabbed, ready, loaded, stages done, stored, end] (%globaltimer ns)
+        const bool tracing = p.trace && lead && task < p.trace_cap;
+        auto stamp = [&](int k) {
+            if (!tracing) return;
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.trace[(size_t)task * kTraceFields + k] = (long long)t;
+        };
+        if (tracing) {
+            unsigned long long smid;
+            asm volatile("{ .reg .u32 s; mov.u32 s, %%smid; cvt.u64.u32 %0, s; }" : "=l"(smid));
+            p.trace[(size_t)task * kTraceFields + 0] = (long long)smid;
+            p.trace[(size_t)task * kTraceFields + 1] = (long long)tr0;
+        }
+        stamp(2);
+        if (seg == 0)
+            load_image_nl<HOT>(v, &p, pix, img);
+        else
+            load_state_nl<HOT>(v, &p, pix, img, !inited, reads_xs(first + k0 % nst));
+        inited = true;
         team_sync(gk);
+        stamp(3);
 
         Stats st{};
         st.timing = p.stats != nullptr;
@@ -2015,14 +2124,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         int pc = 2;   // worklist pass counter (stamps are its low byte; marks start at 0)
         if (p.mode == MODE_HASF) {
             // stage table: (thin, xmode, save_xs) for S1/S3 (cutting) and S5/S7 (filling)
-            const int first = p.do_cut ? 0 : 2, last = p.do_fill ? 3 : 1;
-            for (int r = p.r_first; r <= p.r_last; ++r) {
-                for (int stg = first; stg <= last; ++stg) {
-                    const bool thin = stg == 0 || stg == 3;
-                    const int xmode = (stg == 1 || stg == 3) ? 2 : ((stg == 0 ? has_k : has_a) ? 1 : 0);
-                    const bool save = stg == 0 || stg == 2;
-                    run_stage<FG, HOT>(v, gk, r, thin, xmode, save, sh, cur, p.err, st, pc);
-                }
+            for (int k = k0; k < k1; ++k) {
+                const int r = p.r_first + k / nst, stg = first + k % nst;
+                const bool thin = stg == 0 || stg == 3;
+                const int xmode = (stg == 1 || stg == 3) ? 2 : ((stg == 0 ? has_k : has_a) ? 1 : 0);
+                const bool save = stg == 0 || stg == 2;
+                run_stage<FG, HOT>(v, gk, r, thin, xmode, save, sh, cur, p.err, st, pc);
             }
         } else {
             const int t = p.mode == MODE_THIN ? 1 : 0;
@@ -2031,37 +2138,50 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             engine<FG, HOT>(v, t, p.max_sweeps, sh, cur, p.err, st, pc);
         }
 
-        store_image_nl<HOT>(v, p.out + pix,
-                            p.packed_io ? reinterpret_cast<uint32_t *>(p.out) + (size_t)img * p.H * p.WW : nullptr);
-        if (lead && p.stats) {
-            long long *sp = p.stats + (size_t)img * kStatFields;
+        stamp(4);
+        const bool final_seg = seg == nseg - 1;
+        if (final_seg)
+            store_image_nl<HOT>(v, p.out + pix,
+                                p.packed_io ? reinterpret_cast<uint32_t *>(p.out) + (size_t)img * p.H * p.WW : nullptr);
+        else
+            store_state_nl<HOT>(v, p.xbuf + (size_t)img * 2 * p.H * p.WW, reads_xs(first + k1 % nst));
+        stamp(5);
+        if (lead && p.stats) {   // accumulated over the image's segments (zeroed buffer)
+            unsigned long long *sp = reinterpret_cast<unsigned long long *>(p.stats + (size_t)img * kStatFields);
             const EngineIO eio = *const_cast<const EngineIO *>(&sh.eio);
-            sp[0] = eio.sweeps;
-            sp[1] = eio.passes;
-            sp[2] = eio.calls;
-            sp[3] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.flips);
-            sp[4] = st.cyc_prep;
-            sp[5] = eio.cyc_jacobi;
-            sp[6] = eio.cyc_update;
-            sp[7] = clock64() - t_img0;
-            sp[8] = eio.cyc_tiny;
-            sp[9] = eio.n_tiny;
-            sp[10] = eio.pass_tiny;
-            sp[11] = eio.cyc_dense;
-            sp[12] = eio.n_dense;
-            sp[13] = eio.pass_dense;
-            sp[14] = st.cyc_rank;
-            sp[15] = (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.evals);
+            auto add = [&](int k, long long x) { atomicAdd(sp + k, (unsigned long long)x); };
+            add(0, eio.sweeps);
+            add(1, eio.passes);
+            add(2, eio.calls);
+            add(3, (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.flips));
+            add(4, st.cyc_prep);
+            add(5, eio.cyc_jacobi);
+            add(6, eio.cyc_update);
+            add(7, clock64() - t_img0);
+            add(8, eio.cyc_tiny);
+            add(9, eio.n_tiny);
+            add(10, eio.pass_tiny);
+            add(11, eio.cyc_dense);
+            add(12, eio.n_dense);
+            add(13, eio.pass_dense);
+            add(14, st.cyc_rank);
+            add(15, (long long)*reinterpret_cast<volatile unsigned long long *>(&sh.evals));
             for (int k = 0; k < 4; ++k) {
-                sp[16 + k] = *reinterpret_cast<volatile long long *>(&sh.sstat[k]);
-                sp[20 + k] = *reinterpret_cast<volatile long long *>(&sh.dtime[k]);
-                sp[24 + k] = *reinterpret_cast<volatile long long *>(&sh.bstat[k]);
-                sp[28 + k] = *reinterpret_cast<volatile long long *>(&sh.xstat[k]);
-                sp[32 + k] = *reinterpret_cast<volatile long long *>(&sh.ystat[k]);
+                add(16 + k, *reinterpret_cast<volatile long long *>(&sh.sstat[k]));
+                add(20 + k, *reinterpret_cast<volatile long long *>(&sh.dtime[k]));
+                add(24 + k, *reinterpret_cast<volatile long long *>(&sh.bstat[k]));
+                add(28 + k, *reinterpret_cast<volatile long long *>(&sh.xstat[k]));
+                add(32 + k, *reinterpret_cast<volatile long long *>(&sh.ystat[k]));
             }
         }
         team_sync(gk);
-        if (p.done && lead) {   // all the image's output stored: publish it to the copy-out stream
+        stamp(6);
+        if (!final_seg && lead) {   // image state stored by the whole CTA (barrier above): publish it
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.progress + img), "r"((unsigned)(seg + 1))
+                         : "memory");
+        }
+        if (final_seg && p.done && lead) {   // all the image's output stored: publish it to the copy-out stream
             __threadfence_system();
             atomicAdd(p.done + img / p.chunk, 1u);
         }

@@ -22,6 +22,13 @@ constexpr int kFusedMaxR = 8;
 #endif
 constexpr int kHasfThreads = TS_THREADS;
 
+// most segments per image of the segmented scheduler (4 stages per radius, r <= 16)
+constexpr int kMaxSegs = 64;
+
+// debug task trace: SM id, then %globaltimer ns when the task was taken, its
+// input ready, loaded, its stages done, its result stored, finished
+constexpr int kTraceFields = 7;
+
 // bytes reserved per team control block (teams of > 1 CTA per image)
 constexpr int kTeamCtlBytes = 8192;
 
@@ -110,6 +117,18 @@ struct KParams {
     int chunk;
     int fused;              // 1: fused prep + E-pass allowed (the planner left out the R planes)
     int packed_io;          // 1: in / out are [n][H][WW] uint32 bit rows (host-packed, validated)
+    // segmented scheduling (batches larger than one wave, single-CTA images):
+    // an image's stage list is cut into nseg segments (see seg_range);
+    // the queue hands out (segment, image) tasks segment-major, the image's
+    // bit-plane passes between segments through xbuf ([n][H][WW] words), and
+    // progress[i] counts image i's completed segments (a task waits for its
+    // predecessor).  nseg == 1: whole images.
+    int nseg;
+    int seg_stages, seg_fine;   // segments of seg_stages stages, the last seg_fine stages one each
+    uint32_t *xbuf;         // [n][2][H][WW]: the image, and XS when the next stage reads it
+    unsigned *progress;
+    long long *trace;       // debug: per task kTraceFields int64 (see hasf_kernel) or null
+    long long trace_cap;    // tasks recorded
     int *err;               // first error code (atomicCAS from 0)
     long long *stats;       // [n][kStatFields] (or null), see kStatFields
 };

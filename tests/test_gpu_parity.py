@@ -414,3 +414,53 @@ def test_c2_full_batch_bit_exact():
     for i in (1, 7, 19, 31):
         assert _sha(imgs[i]) == str(z[f"c2_{i}_in_sha"]), f"generator drift on c2[{i}]"
         assert _sha(out[i]) == str(z[f"c2_{i}_out_sha"]), f"c2[{i}]: " + _first_mismatch(out[i], z[f"c2_{i}_out_bits"])
+
+
+def test_segmented_scheduler_large_batch():
+    """A c4 batch larger than one wave (600 images of 256^2, (4,8)) runs as
+    (segment, image) tasks: identical to whole-image tasks, and to the oracle."""
+    lib = _lib.load()
+    imgs = torch.from_numpy(W.config_batch("c4", 4200, 600)).cuda()
+    got = P.hasf_batch(imgs, 4, P.ADJ_48)
+    old = lib.ts_set_segment_stages(0)
+    try:
+        whole = P.hasf_batch(imgs, 4, P.ADJ_48)
+    finally:
+        lib.ts_set_segment_stages(old)
+    assert torch.equal(got, whole)
+    sel = [0, 1, 299, 300, 599]
+    host = imgs.cpu().numpy()[sel]
+    assert np.array_equal(got.cpu().numpy()[sel], O.hasf_batch(host, 4, 4, threads=5))
+
+
+@pytest.mark.parametrize("seg,fine", [(1, 0), (3, 1), (4, 2), (2, 5), (5, 0)])
+def test_segmented_scheduler_forced_vs_oracle(seg, fine):
+    """Forced segmentation on batches smaller than one wave: every task after
+    the first of an image waits for its predecessor on another SM (the image
+    and, mid-radius, the saved plane XS pass through global memory).  Both
+    adjacencies, keep / avoid, radii 1..6, the streamed host entry."""
+    lib = _lib.load()
+    olds = (lib.ts_set_segment_stages(seg), lib.ts_set_segment_fine(fine), lib.ts_set_segment_force(1))
+    try:
+        rng = np.random.default_rng(900 + seg * 10 + fine)
+        for (h, w, fg, r) in [(96, 64, 8, 3), (128, 128, 4, 4), (70, 90, 8, 6), (33, 31, 4, 1)]:
+            imgs = np.stack([random_image(rng, h, w, rng.uniform(0.3, 0.7)) for _ in range(6)])
+            adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+            assert np.array_equal(P.hasf_batch(imgs, r, adj), O.hasf_batch(imgs, r, fg, threads=6)), (h, w, r)
+            keep = (imgs & (rng.random(imgs.shape) < 0.03)).astype(np.uint8)
+            avoid = ((rng.random(imgs.shape) < 0.03) & (imgs == 0)).astype(np.uint8)
+            assert np.array_equal(P.hasf_batch(imgs, r, adj, keep=keep, avoid=avoid),
+                                  O.hasf_batch(imgs, r, fg, keep=keep, avoid=avoid, threads=6)), (h, w, r)
+        imgs = W.config_batch("c1", 1400, 20)
+        want = O.hasf_batch(imgs, 5, 8, threads=8)
+        assert np.array_equal(P.hasf_batch(imgs, 5), want)
+        out = np.zeros_like(imgs)
+        _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, 20, 512, 512, 5, 8, None, None,
+                                          torch.cuda.current_stream().cuda_stream))
+        assert np.array_equal(out, want)
+        _, st = P.hasf_batch(imgs[:3], 5, stats=True)   # stats accumulate over the segments
+        assert (st[:, 2] == 20).all()
+    finally:
+        lib.ts_set_segment_stages(olds[0])
+        lib.ts_set_segment_fine(olds[1])
+        lib.ts_set_segment_force(olds[2])

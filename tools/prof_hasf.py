@@ -41,6 +41,7 @@ def main():
         _lib.load().ts_set_team_size(args.team)
     if args.threads > 0:
         _lib.load().ts_set_cta_threads(args.threads)
+    args.n = args.n or cfg.n
     imgs = torch.from_numpy(W.config_batch(cfg, args.start, args.n)).cuda()
     adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
     plan = np.zeros(6, np.int64)
