@@ -77,56 +77,88 @@ def traffic_from_profiles(cfg_name):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    ~2 ms on a background thread; mark(True/False) brackets the timed region
+    and summary() reports the samples taken inside it (falls back to
+    nvidia-smi -lms 10 when NVML is unavailable)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index=0):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []        # (in_timed_region, sm_mhz, reasons)
+        self.max_mhz = None
+        self.inside = False
+        self.stop = threading.Event()
+        self.t = None
+        self.source = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = [(nm, getattr(N, attr)) for nm, attr in self.REASONS if hasattr(N, attr)]
+
+            def run():
+                while not self.stop.is_set():
+                    try:
+                        mhz = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
+                        self.samples.append((self.inside, mhz, [nm for nm, b in bits if r & b]))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.source = "nvml (2 ms)"
         except Exception:
-            self.proc = None
+            run = self._smi
+            self.source = "nvidia-smi -lms 10"
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+        time.sleep(0.05)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                     "--format=csv,noheader,nounits", "-lms", "10"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in proc.stdout:
+            if self.stop.is_set():
+                break
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                mhz, self.max_mhz = float(parts[0]), float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            self.samples.append((self.inside, mhz, [nm for nm, v in zip(names, parts[2:6])
+                                                    if v.lower().startswith("active")]))
+        proc.terminate()
+
+    def mark(self, inside):
+        self.inside = inside
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.t:
+            self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [s for s in self.samples if s[0]]
+        sm = [s[1] for s in inside]
+        reasons = sorted({r for s in inside for r in s[2]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": self.source}
 
 
 def dist_env():
@@ -374,12 +406,14 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        clk.mark(True)
         for i in range(args.steps):
             flush.fill_(i & 0xFF)          # evict L2 between timed steps (not timed)
             starts[i].record(stream)
             step()
             ends[i].record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
         if world > 1:
             dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -430,6 +464,12 @@ def main():
     wall_ms = (time.perf_counter() - t0) * 1e3
     assert np.array_equal(hout.numpy(), out.cpu().numpy())
     e2e_value = cfg.n * world * e2e_steps / (e2e_ms / 1e3)
+    # bytes that actually cross the host link per step (ts_hasf_batch_host):
+    # the default streamed entry bit-packs on the host (32 px per uint32 word)
+    # for images up to 1024^2 without constraints; otherwise uint8 planes
+    packed = args.host_streaming == 1 and cfg.h * cfg.w <= 1024 * 1024
+    link_bytes = cfg.n * cfg.h * ((cfg.w + 31) // 32) * 4 if packed else cfg.n * cfg.h * cfg.w
+    link_fmt = "bit-packed rows (uint32, 32 px/word)" if packed else "uint8 planes"
 
     if rank == 0:
         peak, peak_src = peak_hbm()
@@ -466,9 +506,10 @@ def main():
                          "algorithmic_bytes_per_launch": bpi * cfg.n,
                          "bytes_model": "32*r_max*H*W per image (SURVEY §8d: 8 stages/radius x 4 B/px)",
                          "kernel": "ts::hasf_kernel (one launch per step)"},
-            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": cfg.n * cfg.h * cfg.w,
-                    "d2h_bytes_per_step": cfg.n * cfg.h * cfg.w, "wall_ms": wall_ms,
-                    "path": E2E_PATH[args.host_streaming != 0]},
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": link_bytes,
+                    "d2h_bytes_per_step": link_bytes, "wall_ms": wall_ms,
+                    "host_uint8_bytes_per_step": {"read": cfg.n * cfg.h * cfg.w, "written": cfg.n * cfg.h * cfg.w},
+                    "link_format": link_fmt, "path": E2E_PATH[args.host_streaming != 0]},
             "gpu_launches": args.steps,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

@@ -170,7 +170,7 @@ int32_t ts_set_fused_prep(int32_t on);
  * filling, each a prep + engine call), segment-major, so the SMs left idle
  * when the queue drains wait for at most one segment instead of one whole
  * image.  The image's bit-plane passes between segments through global
- * memory; results are identical.  0 = whole images; default 4 (one radius;
+ * memory; results are identical.  0 = whole images; default 8 (two radii;
  * env TS_SEG_STAGES overrides at load).  Returns the previous value. */
 int32_t ts_set_segment_stages(int32_t stages);
 
@@ -178,6 +178,13 @@ int32_t ts_set_segment_stages(int32_t stages);
  * segments (the queue's drain then waits for at most one short stage);
  * default 2 (env TS_SEG_FINE).  Returns the previous value. */
 int32_t ts_set_segment_fine(int32_t stages);
+
+/* Tuning / A-B: the segmentation used by the streamed host entry
+ * (ts_hasf_batch_host), whose copy-back and host unpacking overlap the
+ * kernel only while images keep completing, so it prefers coarser segments;
+ * default 8 stages, fine 0 (env TS_SEG_STAGES_HOST / TS_SEG_FINE_HOST).
+ * Returns the previous stage count. */
+int32_t ts_set_host_segments(int32_t stages, int32_t fine);
 
 /* Testing: 1 = segment batches of any size (tasks then often wait for their
  * predecessor segment on another SM).  Returns the previous value. */

@@ -52,6 +52,7 @@ SIGNATURES = {
     "ts_set_segment_stages": ([_i32], _i32),
     "ts_set_segment_fine": ([_i32], _i32),
     "ts_set_segment_force": ([_i32], _i32),
+    "ts_set_host_segments": ([_i32, _i32], _i32),
     "ts_set_trace": ([_vp, _i64], None),
     "ts_hasf_plan": ([_i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int),
 }

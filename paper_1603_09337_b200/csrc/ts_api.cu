@@ -133,9 +133,18 @@ std::atomic<long long> g_trace_cap{0};
 // radius (one cutting or one filling), the image state between them is one plane
 std::atomic<int> g_seg_stages{[] {
     const char *e = getenv("TS_SEG_STAGES");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 8;
 }()};
 std::atomic<int> g_seg_force{0};   // tests: segment batches of any size
+// the streamed host entry's segmentation (env TS_SEG_STAGES_HOST / TS_SEG_FINE_HOST)
+std::atomic<int> g_seg_stages_host{[] {
+    const char *e = getenv("TS_SEG_STAGES_HOST");
+    return e ? atoi(e) : 8;
+}()};
+std::atomic<int> g_seg_fine_host{[] {
+    const char *e = getenv("TS_SEG_FINE_HOST");
+    return e ? atoi(e) : 0;
+}()};
 // the last g_seg_fine stages run as one-stage segments (env TS_SEG_FINE)
 std::atomic<int> g_seg_fine{[] {
     const char *e = getenv("TS_SEG_FINE");
@@ -408,7 +417,10 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     const int total_stages = mode == MODE_HASF ? (r_last - r_first + 1) * nst : 0;
     // segments of seg_stages stages, the last `fine` stages one per segment
     // (the tail when the queue drains is then at most one short stage)
-    const int seg_stages = g_seg_stages.load(), fine = std::max(0, g_seg_fine.load());
+    // (the streamed host entry prefers coarser segments: its copy-back and host
+    // unpacking overlap the kernel only while images keep completing)
+    const int seg_stages = ready ? g_seg_stages_host.load() : g_seg_stages.load();
+    const int fine = std::max(0, ready ? g_seg_fine_host.load() : g_seg_fine.load());
     int nseg = 1;
     if (mode == MODE_HASF && team == 1 && seg_stages > 0 && (n > pl.per_wave || g_seg_force.load()) &&
         total_stages > 1)
@@ -873,6 +885,11 @@ int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
 int32_t ts_set_segment_stages(int32_t stages) { return g_seg_stages.exchange(stages < 0 ? 0 : stages); }
 
 int32_t ts_set_segment_fine(int32_t stages) { return g_seg_fine.exchange(stages < 0 ? 0 : stages); }
+
+int32_t ts_set_host_segments(int32_t stages, int32_t fine) {
+    g_seg_fine_host.store(fine < 0 ? 0 : fine);
+    return g_seg_stages_host.exchange(stages < 0 ? 0 : stages);
+}
 
 int32_t ts_set_segment_force(int32_t on) { return g_seg_force.exchange(on ? 1 : 0); }
 

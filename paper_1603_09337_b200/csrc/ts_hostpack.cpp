@@ -49,10 +49,16 @@ __attribute__((target("avx2"))) void unpack_row_avx2(const uint32_t *s, uint8_t 
     const __m256i sel = _mm256_set1_epi64x((long long)0x8040201008040201ULL);
     const __m256i one = _mm256_set1_epi8(1);
     int x = 0;
+    // the output (8x the input) is written once and not read back here:
+    // non-temporal stores skip the read-for-ownership of every line
+    const bool aligned = (reinterpret_cast<uintptr_t>(d) & 31) == 0;
     for (; (x + 1) * 32 <= w; ++x) {
         const __m256i b = _mm256_shuffle_epi8(_mm256_set1_epi32((int)s[x]), route);
         const __m256i m = _mm256_cmpeq_epi8(_mm256_and_si256(b, sel), sel);
-        _mm256_storeu_si256(reinterpret_cast<__m256i *>(d + 32 * x), _mm256_and_si256(m, one));
+        if (aligned)
+            _mm256_stream_si256(reinterpret_cast<__m256i *>(d + 32 * x), _mm256_and_si256(m, one));
+        else
+            _mm256_storeu_si256(reinterpret_cast<__m256i *>(d + 32 * x), _mm256_and_si256(m, one));
     }
     if (x < ww)
         for (int c = 32 * x; c < w; ++c) d[c] = (uint8_t)((s[x] >> (c - 32 * x)) & 1u);
@@ -122,6 +128,9 @@ void unpack_images(const uint32_t *in, uint8_t *out, int64_t n, int h, int w, in
         unpack_row_scalar(s, d, w, ww);
 #endif
     }
+#if defined(__x86_64__)
+    _mm_sfence();   // the streamed stores are globally visible before the caller returns
+#endif
 }
 
 }  // namespace ts

@@ -440,7 +440,8 @@ def test_segmented_scheduler_forced_vs_oracle(seg, fine):
     and, mid-radius, the saved plane XS pass through global memory).  Both
     adjacencies, keep / avoid, radii 1..6, the streamed host entry."""
     lib = _lib.load()
-    olds = (lib.ts_set_segment_stages(seg), lib.ts_set_segment_fine(fine), lib.ts_set_segment_force(1))
+    olds = (lib.ts_set_segment_stages(seg), lib.ts_set_segment_fine(fine), lib.ts_set_segment_force(1),
+            lib.ts_set_host_segments(seg, fine))
     try:
         rng = np.random.default_rng(900 + seg * 10 + fine)
         for (h, w, fg, r) in [(96, 64, 8, 3), (128, 128, 4, 4), (70, 90, 8, 6), (33, 31, 4, 1)]:
@@ -464,3 +465,4 @@ def test_segmented_scheduler_forced_vs_oracle(seg, fine):
         lib.ts_set_segment_stages(olds[0])
         lib.ts_set_segment_fine(olds[1])
         lib.ts_set_segment_force(olds[2])
+        lib.ts_set_host_segments(olds[3], 0)

@@ -50,3 +50,20 @@ for n in (16, 148, 256):
         assert np.array_equal(hout.numpy(), out.cpu().numpy())
         res.append(f"e2e(streaming={hs}) {te:.3f} ms")
     print("  ".join(res))
+
+# segment settings (the streamed entry's fused launch is segmented too)
+n = 256
+x = torch.from_numpy(imgs).cuda()
+out = torch.empty_like(x)
+hin = torch.from_numpy(imgs).pin_memory()
+hout = torch.empty_like(hin).pin_memory()
+lib.ts_set_host_streaming(1)
+for seg, fine in ((0, 0), (4, 0), (4, 2), (8, 0), (8, 2), (12, 0), (12, 4)):
+    lib.ts_set_segment_stages(seg)
+    lib.ts_set_segment_fine(fine)
+    lib.ts_set_host_segments(seg, fine)
+    tk = timed(lambda: _lib.check(lib.ts_hasf_batch(x.data_ptr(), out.data_ptr(), n, 512, 512, 5, 8, None, None,
+                                                     s.cuda_stream, None)))
+    te = timed(lambda: _lib.check(lib.ts_hasf_batch_host(hin.data_ptr(), hout.data_ptr(), n, 512, 512, 5, 8,
+                                                          None, None, s.cuda_stream)))
+    print(f"seg {seg}:{fine}: kernel {tk:.3f} ms  e2e {te:.3f} ms")
