@@ -138,6 +138,22 @@ int64_t ts_set_smem_budget(int64_t bytes);
  * previous value. */
 int32_t ts_set_dense_divisor(int32_t div);
 
+/* ---- netpbm P4 straight to / from the device bit-row layout -------------
+ * P4 rasters (reference netpbm.py:68-129, the raster bytes after the header):
+ * [n][h][(w + 7) / 8] bytes, 1 bit per pixel, MSB first, rows padded to a
+ * byte, 1 = object; padding bits ignored on read, written as zero.
+ * "rows" = the fused kernel's packed format: [n][h][(w + 31) / 32] uint32,
+ * leftmost pixel in bit 0, padding bits zero. */
+int ts_p4_to_rows(const uint8_t *p4_dev, uint32_t *rows_dev, int64_t n, int32_t h, int32_t w, void *stream);
+int ts_rows_to_p4(const uint32_t *rows_dev, uint8_t *p4_dev, int64_t n, int32_t h, int32_t w, void *stream);
+
+/* HASF on P4 rasters without ever unpacking to bytes: P4 -> bit rows on the
+ * device, the fused kernel reading / writing bit rows, bit rows -> P4.
+ * Replaces read_pbm -> hasf -> write_pbm of cli.run_smooth_command
+ * (cli.py:109-143) for P4 files.  keep/avoid: P4 rasters or NULL. */
+int ts_hasf_batch_p4(const uint8_t *p4_in_dev, uint8_t *p4_out_dev, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                     int32_t fg, const uint8_t *keep_p4_dev, const uint8_t *avoid_p4_dev, void *stream);
+
 /* Tuning/testing: CTAs cooperating on one image (0 = automatic: teams only for
  * images whose hot planes exceed one SM's shared memory and when there are
  * fewer images than co-resident CTAs).  Returns the previous value. */

@@ -43,6 +43,9 @@ SIGNATURES = {
     "ts_connectivity_tables": ([_vp, _vp, _vp, _vp], ctypes.c_int),
     "ts_component_counts_batch": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int),
     "ts_selftest_circuit": ([_vp, _vp], ctypes.c_int),
+    "ts_p4_to_rows": ([_vp, _vp, _i64, _i32, _i32, _vp], ctypes.c_int),
+    "ts_rows_to_p4": ([_vp, _vp, _i64, _i32, _i32, _vp], ctypes.c_int),
+    "ts_hasf_batch_p4": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp], ctypes.c_int),
     "ts_set_smem_budget": ([_i64], _i64),
     "ts_set_dense_divisor": ([_i32], _i32),
     "ts_set_team_size": ([_i32], _i32),

@@ -32,6 +32,9 @@ cudaError_t launch_edt_phase2(const long long *g, void *out, long long *stk, int
 cudaError_t launch_classify(const uint8_t *pix, uint8_t *out, int n, int H, int W, const uint8_t *lut,
                             cudaStream_t st);
 cudaError_t launch_selftest_circuit(uint8_t *out84, uint8_t *out48, cudaStream_t st);
+cudaError_t launch_p4_to_rows(const uint8_t *p4, uint32_t *rows, long long nrows, int w, cudaStream_t st);
+cudaError_t launch_rows_to_p4(const uint32_t *rows, uint8_t *p4, long long nrows, int w, cudaStream_t st);
+cudaError_t launch_p4_to_u8(const uint8_t *p4, uint8_t *out, long long nrows, int w, cudaStream_t st);
 cudaError_t launch_ccl(const uint8_t *img, int *parent, long long *counts, int n, int h, int w, int conn,
                        int target, int exterior, cudaStream_t st);
 }  // namespace ts
@@ -1130,6 +1133,69 @@ int ts_component_counts_batch(const uint8_t *in_dev, int64_t *counts_host, int64
     cudaError_t se = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "component counts");
     if (se != cudaSuccess) return cuda_fail(se, "component counts");
+    return ok();
+}
+
+// ---- netpbm P4 straight into the device bit-row layout (row f2) --------------
+int ts_p4_to_rows(const uint8_t *p4_dev, uint32_t *rows_dev, int64_t n, int32_t h, int32_t w, void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w))) return rc;
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    TS_CUDA(launch_p4_to_rows(p4_dev, rows_dev, n * h, w, st));
+    TS_CUDA(cudaStreamSynchronize(st));
+    return ok();
+}
+
+int ts_rows_to_p4(const uint32_t *rows_dev, uint8_t *p4_dev, int64_t n, int32_t h, int32_t w, void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w))) return rc;
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    TS_CUDA(launch_rows_to_p4(rows_dev, p4_dev, n * h, w, st));
+    TS_CUDA(cudaStreamSynchronize(st));
+    return ok();
+}
+
+int ts_hasf_batch_p4(const uint8_t *p4_in_dev, uint8_t *p4_out_dev, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                     int32_t fg, const uint8_t *keep_p4_dev, const uint8_t *avoid_p4_dev, void *stream) {
+    int rc;
+    if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
+    if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
+    if (n == 0) return ok();
+    cudaStream_t st = (cudaStream_t)stream;
+    const int ww = (w + 31) / 32;
+    const size_t words = (size_t)n * h * ww, px = (size_t)n * h * w;
+    const int nplanes = (keep_p4_dev ? 1 : 0) + (avoid_p4_dev ? 1 : 0);
+    char *ws = nullptr;
+    TS_CUDA(cudaMallocAsync((void **)&ws, 2 * words * 4 + nplanes * px + 64, st));
+    uint32_t *rin = reinterpret_cast<uint32_t *>(ws), *rout = rin + words;
+    uint8_t *k8 = reinterpret_cast<uint8_t *>(rout + words);
+    uint8_t *a8 = keep_p4_dev ? k8 + px : k8;
+    int *err = reinterpret_cast<int *>(ws + ((2 * words * 4 + nplanes * px + 15) & ~(size_t)15));
+    cudaError_t e = cudaMemsetAsync(err, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = launch_p4_to_rows(p4_in_dev, rin, n * h, w, st);
+    if (e == cudaSuccess && keep_p4_dev) e = launch_p4_to_u8(keep_p4_dev, k8, n * h, w, st);
+    if (e == cudaSuccess && avoid_p4_dev) e = launch_p4_to_u8(avoid_p4_dev, a8, n * h, w, st);
+    rc = TS_OK;
+    if (e == cudaSuccess)
+        rc = fused_launch(MODE_HASF, reinterpret_cast<const uint8_t *>(rin), reinterpret_cast<uint8_t *>(rout), n, h, w,
+                          1, r_max, 1, 1, fg, keep_p4_dev ? k8 : nullptr, avoid_p4_dev ? a8 : nullptr, nullptr, -1, st,
+                          nullptr, err, nullptr, nullptr, nullptr, 1, 1);
+    if (e == cudaSuccess && rc == TS_OK) e = launch_rows_to_p4(rout, p4_out_dev, n * h, w, st);
+    int herr = 0;
+    cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    const std::string keep_msg = g_err;
+    cudaFreeAsync(ws, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (rc) {
+        g_err = keep_msg;
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "P4 path");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
+    if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
+    if (herr) return device_error(herr, MODE_HASF);
     return ok();
 }
 

@@ -206,8 +206,55 @@ def gen_hasf_configs():
     np.savez_compressed(os.path.join(HERE, "hasf_configs.npz"), **d)
 
 
+def gen_netpbm():
+    """netpbm.py: bytes the reference writes (P1 / P4 at ragged widths, PGM
+    renderings), what it reads back, and its NetpbmError messages on
+    malformed files."""
+    import tempfile
+    rng = np.random.default_rng(7009)
+    d = {}
+    tmp = tempfile.mkdtemp()
+    path = os.path.join(tmp, "f")
+    cases = [rand_img(rng, h, w, 0.5) for (h, w) in ((1, 1), (3, 7), (5, 8), (9, 13), (17, 40), (31, 70))]
+    for i, img in enumerate(cases):
+        d[f"pbm{i}_img"] = img
+        for fmt in ("P1", "P4"):
+            ts.write_pbm(img, path, format=fmt)
+            d[f"pbm{i}_{fmt}"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+    d["pbm_count"] = np.array(len(cases))
+    dist = ts.edt_squared(rand_img(rng, 12, 9, 0.2))
+    dist_empty = ts.edt_squared(np.zeros((4, 5), np.uint8))
+    for name, m in (("dist", dist), ("empty", dist_empty)):
+        for mode in ("root", "squared"):
+            for fmt in ("P2", "P5"):
+                ts.write_pgm(m, path, mode=mode, format=fmt)
+                d[f"pgm_{name}_{mode}_{fmt}"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+                d[f"pgm_{name}_{mode}_{fmt}_read"] = ts.read_pgm(path)
+        d[f"pgm_{name}_in"] = m
+    bad = [b"P3\n1 1\n0\n", b"P1\n2 2\n0 1 1\n", b"P4\n9 2\n\x00\x00\x00", b"P1\n0 2\n",
+           b"P1\nx 2\n0 1", b"P1\n2 1\n0 2", b"P4\n8 1", b"P1 # c\n2 # c\n1\n01", b"P4\n3 1\n\xe0",
+           b"P4\n3 2 \xff\x00", b"", b"P2\n2 1\n70000\n1 2\n", b"P5\n2 1\n255\n\x01"]
+    msgs, imgs = [], []
+    for raw in bad:
+        open(path, "wb").write(raw)
+        reader = ts.read_pgm if raw[:2] in (b"P2", b"P5") else ts.read_pbm
+        try:
+            out = reader(path)
+            msgs.append("")
+            imgs.append(np.asarray(out, np.int64).reshape(-1))
+        except ts.NetpbmError as e:
+            msgs.append(str(e))
+            imgs.append(np.zeros(0, np.int64))
+    d["bad_count"] = np.array(len(bad))
+    for i, (raw, m, im) in enumerate(zip(bad, msgs, imgs)):
+        d[f"bad{i}_raw"] = np.frombuffer(raw, np.uint8)
+        d[f"bad{i}_msg"] = np.array(m)
+        d[f"bad{i}_out"] = im
+    np.savez_compressed(os.path.join(HERE, "netpbm.npz"), **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["lut", "sep", "edt", "morph", "engine", "halves", "hasf_small", "hasf_configs"]
+    which = sys.argv[1:] or ["lut", "sep", "edt", "morph", "engine", "halves", "hasf_small", "hasf_configs", "netpbm"]
     for name in which:
         t0 = time.perf_counter()
         globals()[f"gen_{name}"]()

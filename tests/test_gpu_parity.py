@@ -466,3 +466,80 @@ def test_segmented_scheduler_forced_vs_oracle(seg, fine):
         lib.ts_set_segment_fine(olds[1])
         lib.ts_set_segment_force(olds[2])
         lib.ts_set_host_segments(olds[3], 0)
+
+
+# ---- netpbm P4 straight into the device layout, CLI on the device (row f2) ----
+def test_p4_rows_round_trip_ragged_widths():
+    lib = _lib.load()
+    rng = np.random.default_rng(4040)
+    st = torch.cuda.current_stream().cuda_stream
+    for w in (1, 7, 8, 9, 31, 32, 33, 100, 513):
+        h, n = 5, 3
+        rb, ww = (w + 7) // 8, (w + 31) // 32
+        img = (rng.random((n, h, w)) < 0.5).astype(np.uint8)
+        p4 = np.packbits(img, axis=2)
+        noisy = p4.copy()
+        if w % 8:
+            noisy[:, :, -1] |= np.uint8((1 << (8 - w % 8)) - 1)   # padding bits set: ignored
+        d_p4 = torch.from_numpy(noisy).cuda()
+        rows = torch.zeros((n, h, ww), dtype=torch.int32, device="cuda")
+        _lib.check(lib.ts_p4_to_rows(d_p4.data_ptr(), rows.data_ptr(), n, h, w, st))
+        r = rows.cpu().numpy().view(np.uint32)
+        bits = ((r[..., None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(n, h, ww * 32)[:, :, :w]
+        assert np.array_equal(bits, img), w
+        assert np.all((r[:, :, -1] >> np.uint32(w - 32 * (ww - 1))) == 0) or w % 32 == 0
+        back = torch.full((n, h, rb), 0xAB, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.ts_rows_to_p4(rows.data_ptr(), back.data_ptr(), n, h, w, st))
+        assert np.array_equal(back.cpu().numpy(), p4), w
+
+
+def test_hasf_p4_matches_hasf():
+    rng = np.random.default_rng(4041)
+    imgs = W.config_batch("c1", 1500, 3)
+    got = P.hasf_p4(np.packbits(imgs, axis=2), 512, 5)
+    assert np.array_equal(np.unpackbits(got, axis=2)[:, :, :512], O.hasf_batch(imgs, 5, 8, threads=3))
+    for (h, w, fg, r) in ((37, 45, 8, 3), (64, 33, 4, 2), (20, 300, 8, 4), (1, 1, 8, 1)):
+        im = np.stack([random_image(rng, h, w, 0.5) for _ in range(4)])
+        keep = (im & (rng.random(im.shape) < 0.05)).astype(np.uint8)
+        avoid = ((rng.random(im.shape) < 0.05) & (im == 0)).astype(np.uint8)
+        adj = P.ADJ_84 if fg == 8 else P.ADJ_48
+        got = P.hasf_p4(np.packbits(im, axis=2), w, r, adj, keep=np.packbits(keep, axis=2),
+                        avoid=np.packbits(avoid, axis=2))
+        want = O.hasf_batch(im, r, fg, keep=keep, avoid=avoid, threads=4)
+        assert np.array_equal(np.unpackbits(got, axis=2)[:, :, :w], want), (h, w)
+        assert np.array_equal(got, np.packbits(want, axis=2))   # padding bits zero
+    bad_keep = np.packbits(np.ones((1, 8, 8), np.uint8), axis=2)
+    with pytest.raises(ValueError, match="keep-constraint pixels must be object pixels"):
+        P.hasf_p4(np.packbits(np.zeros((1, 8, 8), np.uint8), axis=2), 8, 2, keep=bad_keep)
+    big = W.config_batch("c4", 4300, 400)   # > one wave: segmented tasks on bit rows
+    got = P.hasf_p4(np.packbits(big, axis=2), 256, 4, P.ADJ_48)
+    assert np.array_equal(np.unpackbits(got, axis=2), P.hasf_batch(big, 4, P.ADJ_48))
+
+
+def test_cli_smooth_and_benchmark_on_device(tmp_path, capsys):
+    from paper_1603_09337_b200 import cli
+    img = W.jagged_disc(256, 256, 90)
+    src = tmp_path / "in.pbm"
+    for fmt in ("P4", "P1"):
+        P.write_pbm(img, src, format=fmt)
+        out = tmp_path / f"out_{fmt}.pbm"
+        assert cli.main(["smooth", str(src), str(out), "--radius", "4", "--verify", "--device", "cuda"]) == 0
+        err = capsys.readouterr().err
+        fb = [int(t) for t in err.split() if t.isdigit()]
+        assert len(fb) == 4 and fb[0] == fb[1] and fb[2] == fb[3], err
+        assert out.read_bytes()[:2] == fmt.encode()
+        assert np.array_equal(P.read_pbm(out), O.hasf(img, 4, 8))
+    P.write_pbm(img, src)
+    assert cli.main(["smooth", str(src), str(tmp_path / "z.pbm"), "--radius", "0"]) == 0
+    assert (tmp_path / "z.pbm").read_bytes() == src.read_bytes()
+    keep = (img & (np.arange(img.size).reshape(img.shape) % 97 == 0)).astype(np.uint8)
+    P.write_pbm(keep, tmp_path / "k.pbm")
+    assert cli.main(["smooth", str(src), str(tmp_path / "c.pbm"), "--radius", "5", "--adj", "4,8",
+                     "--constraint-keep", str(tmp_path / "k.pbm")]) == 0
+    res = P.read_pbm(tmp_path / "c.pbm")
+    assert np.array_equal(res, O.hasf(img, 5, 4, keep=keep)) and np.all(res[keep == 1] == 1)
+    capsys.readouterr()
+    assert cli.main(["benchmark", str(src), "--radius", "3", "--workers-list", "1,2", "--reps", "2"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    assert lines[0] == "scheduler,workers,t_min_s,speedup,efficiency" and len(lines) == 3
+    assert lines[1].startswith("nps,1,")
