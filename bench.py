@@ -170,8 +170,11 @@ def dist_env():
 
 def cpu_reference(cfg, images, threads):
     import oracle as O
+    keep = avoid = None
+    if cfg.constraints > 0:
+        keep, avoid = W.constraint_masks(cfg, images)
     t0 = time.perf_counter()
-    O.hasf_batch(images, cfg.r_max, cfg.fg, threads=threads)
+    O.hasf_batch(images, cfg.r_max, cfg.fg, keep=keep, avoid=avoid, threads=threads)
     return time.perf_counter() - t0
 
 
@@ -208,10 +211,10 @@ def _ref_init(path):
 
 
 def _ref_one(job):
-    img, r_max, fg = job
+    img, r_max, fg, keep, avoid = job
     adj = _REF.ADJ_84 if fg == 8 else _REF.ADJ_48
     # reference smoothing.py:187-212, one worker per process
-    return _REF.hasf(img, _REF.SmoothingConfig(r_max=r_max, adj=adj, workers=1))
+    return _REF.hasf(img, _REF.SmoothingConfig(r_max=r_max, adj=adj, keep=keep, avoid=avoid, workers=1))
 
 
 def stock_reference_available():
@@ -292,7 +295,10 @@ def run_reference(args, cfg):
     line_extra = {}
     if ok:
         import multiprocessing as mp
-        jobs = [(im, cfg.r_max, cfg.fg) for im in imgs]
+        ks = avs = [None] * len(imgs)
+        if cfg.constraints > 0:
+            ks, avs = W.constraint_masks(cfg, imgs)
+        jobs = [(im, cfg.r_max, cfg.fg, k_, a_) for im, k_, a_ in zip(imgs, ks, avs)]
         with mp.get_context("fork").Pool(cores, initializer=_ref_init, initargs=(REF_DIR,)) as pool:
             outs = None
             for _ in range(args.warmup):
@@ -306,7 +312,8 @@ def run_reference(args, cfg):
         # the port beside it (not the arm's value): same sample, all host threads
         import oracle as O
         tp = cpu_reference(cfg, imgs, cores)
-        port_out = O.hasf_batch(imgs, cfg.r_max, cfg.fg, threads=cores)
+        port_out = O.hasf_batch(imgs, cfg.r_max, cfg.fg, keep=None if cfg.constraints <= 0 else ks,
+                                avoid=None if cfg.constraints <= 0 else avs, threads=cores)
         same = outs is not None and all(np.array_equal(a, b) for a, b in zip(outs, port_out))
         kind = "reference"
         sample = (f"{desc} per step; unmodified toposmooth 0.1.0 (numba) from baseline/_ref, hasf(workers=1) "
@@ -385,12 +392,20 @@ def main():
     imgs_np = W.config_batch(cfg, rank * cfg.n, cfg.n)
     x = torch.from_numpy(imgs_np).cuda()
     out = torch.empty_like(x)
+    # constrained configs (c1k): seeded keep / avoid control images, resident too
+    keep_np = avoid_np = None
+    if cfg.constraints > 0:
+        keep_np, avoid_np = W.constraint_masks(cfg, imgs_np, rank * cfg.n)
+    kd = None if keep_np is None else torch.from_numpy(keep_np).cuda()
+    ad = None if avoid_np is None else torch.from_numpy(avoid_np).cuda()
+    kp = None if kd is None else kd.data_ptr()
+    ap_ = None if ad is None else ad.data_ptr()
     stream = torch.cuda.current_stream()
     lib = _lib.load()
 
     def step():
         _lib.check(lib.ts_hasf_batch(x.data_ptr(), out.data_ptr(), cfg.n, cfg.h, cfg.w, cfg.r_max, cfg.fg,
-                                     None, None, stream.cuda_stream, None))
+                                     kp, ap_, stream.cuda_stream, None))
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
 
@@ -423,7 +438,7 @@ def main():
 
     # stats + correctness (outside the timed region): topology invariants of
     # every output (device component counts), bit-exactness on a sample
-    _, stats = P.hasf_batch(x, cfg.r_max, adj, stats=True)
+    _, stats = P.hasf_batch(x, cfg.r_max, adj, keep=kd, avoid=ad, stats=True)
     fi, bi = P.topology_counts(x, adj)
     fo, bo = P.topology_counts(out, adj)
     topo_ok = int(np.sum((fi == fo) & (bi == bo)))
@@ -434,8 +449,13 @@ def main():
     if args.verify > 0 and rank == 0 and cfg.h * cfg.w <= 2048 * 2048:
         import oracle as O
         k = min(args.verify, cfg.n, 1 if cfg.h * cfg.w > 512 * 512 else args.verify)
-        want = O.hasf_batch(imgs_np[:k], cfg.r_max, cfg.fg)
-        assert np.array_equal(out[:k].cpu().numpy(), want), "bench output differs from the oracle"
+        want = O.hasf_batch(imgs_np[:k], cfg.r_max, cfg.fg, keep=None if keep_np is None else keep_np[:k],
+                            avoid=None if avoid_np is None else avoid_np[:k])
+        got = out[:k].cpu().numpy()
+        assert np.array_equal(got, want), "bench output differs from the oracle"
+        if keep_np is not None:   # the constraints held on every output
+            o = out.cpu().numpy()
+            assert np.all(o[keep_np == 1] == 1) and np.all(o[avoid_np == 1] == 0)
         verified = k
 
     # e2e through the C ABI host-buffer entry, pinned host memory
@@ -443,10 +463,14 @@ def main():
     lib.ts_set_host_streaming(args.host_streaming)
     hin = torch.from_numpy(imgs_np).pin_memory()
     hout = torch.empty_like(hin).pin_memory()
+    hk = None if keep_np is None else torch.from_numpy(keep_np).pin_memory()
+    ha = None if avoid_np is None else torch.from_numpy(avoid_np).pin_memory()
+    hkp = None if hk is None else hk.data_ptr()
+    hap = None if ha is None else ha.data_ptr()
 
     def e2e_step():
         _lib.check(lib.ts_hasf_batch_host(hin.data_ptr(), hout.data_ptr(), cfg.n, cfg.h, cfg.w, cfg.r_max,
-                                          cfg.fg, None, None, stream.cuda_stream))
+                                          cfg.fg, hkp, hap, stream.cuda_stream))
 
     e2e_step()
     torch.cuda.synchronize()
@@ -465,9 +489,12 @@ def main():
     assert np.array_equal(hout.numpy(), out.cpu().numpy())
     e2e_value = cfg.n * world * e2e_steps / (e2e_ms / 1e3)
     # bytes that actually cross the host link per step (ts_hasf_batch_host):
-    # the default streamed entry bit-packs on the host (32 px per uint32 word)
-    # for images up to 1024^2 without constraints; otherwise uint8 planes
+    # the default streamed entry bit-packs the image and any keep / avoid
+    # planes on the host (32 px per uint32 word) for images up to 1024^2;
+    # otherwise uint8 planes
     packed = args.host_streaming == 1 and cfg.h * cfg.w <= 1024 * 1024
+    planes = 1 + (keep_np is not None) + (avoid_np is not None)   # inputs: image + control images
+    link_in = planes * (cfg.n * cfg.h * ((cfg.w + 31) // 32) * 4 if packed else cfg.n * cfg.h * cfg.w)
     link_bytes = cfg.n * cfg.h * ((cfg.w + 31) // 32) * 4 if packed else cfg.n * cfg.h * cfg.w
     link_fmt = "bit-packed rows (uint32, 32 px/word)" if packed else "uint8 planes"
 
@@ -485,7 +512,8 @@ def main():
                    "sample": f"{desc}, oracle/ C restatement of the reference hasf on {cores} host "
                              f"threads, {ts_:.1f} s"}
         plan = np.zeros(6, np.int64)
-        lib.ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
+        lib.ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, int(keep_np is not None), int(avoid_np is not None),
+                         plan.ctypes.data)
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -494,6 +522,9 @@ def main():
             "config": {"workload": f"{cfg.name}: {cfg.n}x{cfg.h}x{cfg.w} per GPU, r_max={cfg.r_max}, "
                                    f"({cfg.fg},{12 - cfg.fg})", "global_batch": cfg.n * world,
                        "image": [cfg.h, cfg.w], "r_max": cfg.r_max, "adjacency": [cfg.fg, 12 - cfg.fg],
+                       "constraints": (None if cfg.constraints <= 0 else
+                                       f"seeded keep / avoid control images, {cfg.constraints:.0%} of object / "
+                                       f"background pixels (W.constraint_masks)"),
                        "parallelism": f"images sharded over {world} GPU(s), no collective",
                        "l2": "flushed between timed steps (256 MiB fill, not timed); per-step CUDA events",
                        "plan": {"ctas_per_wave": int(plan[0]), "ctas_per_sm": int(plan[1]),
@@ -506,9 +537,10 @@ def main():
                          "algorithmic_bytes_per_launch": bpi * cfg.n,
                          "bytes_model": "32*r_max*H*W per image (SURVEY §8d: 8 stages/radius x 4 B/px)",
                          "kernel": "ts::hasf_kernel (one launch per step)"},
-            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": link_bytes,
+            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": link_in,
                     "d2h_bytes_per_step": link_bytes, "wall_ms": wall_ms,
-                    "host_uint8_bytes_per_step": {"read": cfg.n * cfg.h * cfg.w, "written": cfg.n * cfg.h * cfg.w},
+                    "host_uint8_bytes_per_step": {"read": planes * cfg.n * cfg.h * cfg.w,
+                                                  "written": cfg.n * cfg.h * cfg.w},
                     "link_format": link_fmt, "path": E2E_PATH[args.host_streaming != 0]},
             "gpu_launches": args.steps,
             "cpu_baseline": cpu,

@@ -167,8 +167,8 @@ int32_t ts_set_cta_threads(int32_t threads);
  * on host threads (8x fewer bytes over the host link) and ONE fused launch
  * starts while the packed chunks are still being copied (stream memory
  * operations gate each image on its chunk and each chunk's copy-back on its
- * images); the results are unpacked on the host chunk by chunk; calls with
- * keep / avoid planes stream the uint8 planes (as 2); 2 = streamed uint8
+ * images); the results are unpacked on the host chunk by chunk; keep /
+ * avoid planes are bit-packed and streamed the same way; 2 = streamed uint8
  * chunks, no host packing; 0 = the chunked pipeline of separate launches
  * (always used under a serialising profiler -- ncu / nsys injection --
  * or CUDA_LAUNCH_BLOCKING=1).  Returns the previous value. */

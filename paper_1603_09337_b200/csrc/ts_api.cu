@@ -34,7 +34,6 @@ cudaError_t launch_classify(const uint8_t *pix, uint8_t *out, int n, int H, int 
 cudaError_t launch_selftest_circuit(uint8_t *out84, uint8_t *out48, cudaStream_t st);
 cudaError_t launch_p4_to_rows(const uint8_t *p4, uint32_t *rows, long long nrows, int w, cudaStream_t st);
 cudaError_t launch_rows_to_p4(const uint32_t *rows, uint8_t *p4, long long nrows, int w, cudaStream_t st);
-cudaError_t launch_p4_to_u8(const uint8_t *p4, uint8_t *out, long long nrows, int w, cudaStream_t st);
 cudaError_t launch_ccl(const uint8_t *img, int *parent, long long *counts, int n, int h, int w, int conn,
                        int target, int exterior, cudaStream_t st);
 }  // namespace ts
@@ -429,7 +428,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
         total_stages > 1)
         nseg = seg_count(total_stages, seg_stages, fine);
     const size_t ws_words = (size_t)pl.stride_ws * (team > 1 ? teams : grid);
-    const size_t xbuf_words = nseg > 1 ? (size_t)n * 2 * h * pl.WW : 0;
+    const size_t xbuf_words = nseg > 1 ? (size_t)n * 4 * h * pl.WW : 0;   // image, XS, keep, avoid
     const size_t tctl_bytes = team > 1 ? (size_t)teams * kTeamCtlBytes : 0;
     const size_t stats_bytes = stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0;
     const size_t prog_bytes = nseg > 1 ? (((size_t)n * sizeof(unsigned) + 63) & ~(size_t)63) : 0;
@@ -746,7 +745,7 @@ int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
 // buffers are cached per process (one streamed call at a time holds them).
 std::mutex g_stage_mu;
 struct Stage {
-    uint32_t *in = nullptr, *out = nullptr;
+    uint32_t *in = nullptr, *out = nullptr;   // in: image, keep, avoid planes (words each)
     size_t words = 0;
 } g_stage;
 
@@ -779,14 +778,15 @@ int stage_reserve(size_t words) {
     if (g_stage.in) cudaFreeHost(g_stage.in);
     if (g_stage.out) cudaFreeHost(g_stage.out);
     g_stage = Stage{};
-    TS_CUDA(cudaHostAlloc((void **)&g_stage.in, words * 4, cudaHostAllocDefault));
+    TS_CUDA(cudaHostAlloc((void **)&g_stage.in, 3 * words * 4, cudaHostAllocDefault));
     TS_CUDA(cudaHostAlloc((void **)&g_stage.out, words * 4, cudaHostAllocDefault));
     g_stage.words = words;
     return TS_OK;
 }
 
 int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int32_t h, int32_t w,
-                              int32_t r_max, int32_t fg, cudaStream_t user, const MemOps &mo) {
+                              int32_t r_max, int32_t fg, const uint8_t *keep_host, const uint8_t *avoid_host,
+                              cudaStream_t user, const MemOps &mo) {
     const int ww = (w + 31) / 32;
     const size_t img = (size_t)h * w, wimg = (size_t)h * ww, words = (size_t)n * wimg;
     int64_t chunk = std::max<int64_t>(1, (int64_t)(chunk_bytes() / std::max<size_t>(img, 1)));
@@ -796,8 +796,17 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
     int rc = stage_reserve(words);
     if (rc) return rc;
     uint32_t *hin = g_stage.in, *hout = g_stage.out;
+    uint32_t *hk = keep_host ? g_stage.in + g_stage.words : nullptr;
+    uint32_t *ha = avoid_host ? g_stage.in + 2 * g_stage.words : nullptr;
+    // pack (and validate) chunk k of the image and the constraint planes
+    auto pack_chunk = [&](int64_t i0, int64_t cnt) {
+        bool good = pack_images(in_host + i0 * img, hin + i0 * wimg, cnt, h, w, ww);
+        if (hk) good = pack_images(keep_host + i0 * img, hk + i0 * wimg, cnt, h, w, ww) && good;
+        if (ha) good = pack_images(avoid_host + i0 * img, ha + i0 * wimg, cnt, h, w, ww) && good;
+        return good;
+    };
     // chunk 0 packed (and validated) before anything is enqueued
-    if (!pack_images(in_host, hin, std::min<int64_t>(chunk, n), h, w, ww))
+    if (!pack_chunk(0, std::min<int64_t>(chunk, n)))
         return fail(TS_ERR_VALUE, "binary image pixels must be 0 or 1");   // grid.py:60-61
     int dev = 0;
     TS_CUDA(cudaGetDevice(&dev));
@@ -805,13 +814,14 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
     if ((rc = host_ctx(dev, hc))) return rc;
     uint32_t *d = nullptr;
     int *err = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&d, words * 4 * 2, user));
+    TS_CUDA(cudaMallocAsync((void **)&d, words * 4 * 4, user));
     TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
     TS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), user));
     unsigned *flags = take_flags(dev);
     if (!flags) return fail(TS_ERR_CUDA, "cudaMalloc(chunk flags)");
     TS_CUDA(cudaMemsetAsync(flags, 0, 2 * nchunks * sizeof(unsigned), user));
     uint32_t *din = d, *dout = d + words;
+    uint32_t *dk = keep_host ? d + 2 * words : nullptr, *da = avoid_host ? d + 3 * words : nullptr;
     unsigned *ready = flags, *done = flags + nchunks;
     cudaStream_t sin = hc->sin, sout = hc->sout, sc = hc->sc;
     cudaEvent_t ev0 = hc->ev0, ec = hc->ec;
@@ -825,12 +835,17 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
     auto send = [&](int k) {   // chunk k (already packed): copy, then flag
         const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
         if (!bad) e = cudaMemcpyAsync(din + i0 * wimg, hin + i0 * wimg, cnt * wimg * 4, cudaMemcpyHostToDevice, sin);
+        if (!bad && dk && e == cudaSuccess)
+            e = cudaMemcpyAsync(dk + i0 * wimg, hk + i0 * wimg, cnt * wimg * 4, cudaMemcpyHostToDevice, sin);
+        if (!bad && da && e == cudaSuccess)
+            e = cudaMemcpyAsync(da + i0 * wimg, ha + i0 * wimg, cnt * wimg * 4, cudaMemcpyHostToDevice, sin);
         if (e == cudaSuccess) mrc = mo.write(sin, (unsigned long long)(uintptr_t)(ready + k), 1u, kWriteDefault);
     };
     if (e == cudaSuccess) send(0);
     if (e == cudaSuccess && mrc == 0)
         rc = fused_launch(MODE_HASF, reinterpret_cast<const uint8_t *>(din), reinterpret_cast<uint8_t *>(dout), n, h,
-                          w, 1, r_max, 1, 1, fg, nullptr, nullptr, nullptr, -1, sc, nullptr, err, nullptr, ready, done,
+                          w, 1, r_max, 1, 1, fg, reinterpret_cast<const uint8_t *>(dk),
+                          reinterpret_cast<const uint8_t *>(da), nullptr, -1, sc, nullptr, err, nullptr, ready, done,
                           (int)chunk, 1);
     const bool launched = e == cudaSuccess && mrc == 0 && rc == TS_OK;
     if (launched) {
@@ -845,7 +860,7 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
         // (after a bad chunk the flags are still raised so the launch drains)
         for (int k = 1; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
             const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
-            if (!bad && !pack_images(in_host + i0 * img, hin + i0 * wimg, cnt, h, w, ww)) bad = true;
+            if (!bad && !pack_chunk(i0, cnt)) bad = true;
             send(k);
         }
         // results: unpack chunk k as soon as its copy-back finished
@@ -926,8 +941,8 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
                getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr || (lb && lb[0] == '1');
     }();
     if (!big && !serialised && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR) {
-        if (!keep_host && !avoid_host && g_streamed.load() == 1)
-            return hasf_host_streamed_packed(in_host, out_host, n, h, w, r_max, fg, user, mo);
+        if (g_streamed.load() == 1)
+            return hasf_host_streamed_packed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);
         return hasf_host_streamed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);
     }
     const int nchunks = big ? 1 : (int)std::min<int64_t>(n, 4);
@@ -1165,23 +1180,21 @@ int ts_hasf_batch_p4(const uint8_t *p4_in_dev, uint8_t *p4_out_dev, int64_t n, i
     if (n == 0) return ok();
     cudaStream_t st = (cudaStream_t)stream;
     const int ww = (w + 31) / 32;
-    const size_t words = (size_t)n * h * ww, px = (size_t)n * h * w;
-    const int nplanes = (keep_p4_dev ? 1 : 0) + (avoid_p4_dev ? 1 : 0);
+    const size_t words = (size_t)n * h * ww;
     char *ws = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&ws, 2 * words * 4 + nplanes * px + 64, st));
-    uint32_t *rin = reinterpret_cast<uint32_t *>(ws), *rout = rin + words;
-    uint8_t *k8 = reinterpret_cast<uint8_t *>(rout + words);
-    uint8_t *a8 = keep_p4_dev ? k8 + px : k8;
-    int *err = reinterpret_cast<int *>(ws + ((2 * words * 4 + nplanes * px + 15) & ~(size_t)15));
+    TS_CUDA(cudaMallocAsync((void **)&ws, 4 * words * 4 + 64, st));
+    uint32_t *rin = reinterpret_cast<uint32_t *>(ws), *rout = rin + words, *rk = rout + words, *ra = rk + words;
+    int *err = reinterpret_cast<int *>(ra + words);
     cudaError_t e = cudaMemsetAsync(err, 0, sizeof(int), st);
     if (e == cudaSuccess) e = launch_p4_to_rows(p4_in_dev, rin, n * h, w, st);
-    if (e == cudaSuccess && keep_p4_dev) e = launch_p4_to_u8(keep_p4_dev, k8, n * h, w, st);
-    if (e == cudaSuccess && avoid_p4_dev) e = launch_p4_to_u8(avoid_p4_dev, a8, n * h, w, st);
+    if (e == cudaSuccess && keep_p4_dev) e = launch_p4_to_rows(keep_p4_dev, rk, n * h, w, st);
+    if (e == cudaSuccess && avoid_p4_dev) e = launch_p4_to_rows(avoid_p4_dev, ra, n * h, w, st);
     rc = TS_OK;
-    if (e == cudaSuccess)
+    if (e == cudaSuccess)   // packed_io: image and constraints as bit rows
         rc = fused_launch(MODE_HASF, reinterpret_cast<const uint8_t *>(rin), reinterpret_cast<uint8_t *>(rout), n, h, w,
-                          1, r_max, 1, 1, fg, keep_p4_dev ? k8 : nullptr, avoid_p4_dev ? a8 : nullptr, nullptr, -1, st,
-                          nullptr, err, nullptr, nullptr, nullptr, 1, 1);
+                          1, r_max, 1, 1, fg, keep_p4_dev ? reinterpret_cast<const uint8_t *>(rk) : nullptr,
+                          avoid_p4_dev ? reinterpret_cast<const uint8_t *>(ra) : nullptr, nullptr, -1, st, nullptr, err,
+                          nullptr, nullptr, nullptr, 1, 1);
     if (e == cudaSuccess && rc == TS_OK) e = launch_rows_to_p4(rout, p4_out_dev, n * h, w, st);
     int herr = 0;
     cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);

@@ -1846,6 +1846,23 @@ __device__ __forceinline__ void run_stage(const View &v, const Img &gt, int r, b
     }
 }
 
+// bit rows [H][WW] (host- or P4-packed, or a segment's saved state) into a
+// plane; the strip's words are requested together (one latency per batch)
+__device__ __forceinline__ void load_rows(const Img &g, const uint32_t *from, uint32_t *to) {
+    walk_strips(g, [&](int x, int y0, int y1, int) {
+        constexpr int kB = 16;
+        for (int yb = y0; yb < y1; yb += kB) {
+            uint32_t w[kB];
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (yb + j < y1) w[j] = __ldcg(from + (size_t)(yb + j) * g.WW + x);
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (yb + j < y1) to[pidx(g, yb + j, x)] = w[j];
+        }
+    });
+}
+
 // image prologue: clear planes, pack inputs, validate (all team threads)
 template <bool HOT>
 __device__ __noinline__ void load_image_nl(const View &v, const KParams *pp, size_t pix, int img) {
@@ -1864,14 +1881,17 @@ __device__ __noinline__ void load_image_nl(const View &v, const KParams *pp, siz
     for (int q = tid; q < (g.plen + 15) >> 4; q += nthr)
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
     team_sync(g);
-    if (p.packed_io) {   // host-packed bit rows (validated on the host)
-        const uint32_t *src = reinterpret_cast<const uint32_t *>(p.in) + (size_t)img * g.H * g.WW;
-        for_strip(g, [&](int y, int x, int q) { g.I[q] = src[(size_t)y * g.WW + x]; });
+    const size_t wimg = (size_t)img * g.H * g.WW;
+    if (p.packed_io) {   // bit rows (host- or P4-packed: always binary), constraints too
+        load_rows(g, reinterpret_cast<const uint32_t *>(p.in) + wimg, g.I);
     } else {
         pack_plane(p.in + pix, g.I, g, p.err, ERR_NOT_BINARY);
     }
     if (p.mode == MODE_THIN || p.mode == MODE_THICKEN) {
         pack_plane(p.keep + pix, g.B, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+    } else if (p.packed_io) {
+        if (has_k) load_rows(g, reinterpret_cast<const uint32_t *>(p.keep) + wimg, g.K);
+        if (has_a) load_rows(g, reinterpret_cast<const uint32_t *>(p.avoid) + wimg, g.A);
     } else {
         if (has_k) pack_plane(p.keep + pix, g.K, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
         if (has_a) pack_plane(p.avoid + pix, g.A, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
@@ -1920,36 +1940,31 @@ __device__ __noinline__ void load_state_nl(const View &v, const KParams *pp, siz
         reinterpret_cast<uint4 *>(g.mark)[q] = make_uint4(0, 0, 0, 0);
     if (clear) team_sync(g);
     const size_t wimg = (size_t)g.H * g.WW;
-    const uint32_t *src = p.xbuf + (size_t)img * 2 * wimg;
-    // the strip's words are requested together (L2 latency paid once per batch)
-    auto copy_in = [&](const uint32_t *from, uint32_t *to) {
-        walk_strips(g, [&](int x, int y0, int y1, int) {
-            constexpr int kB = 16;
-            for (int yb = y0; yb < y1; yb += kB) {
-                uint32_t w[kB];
-#pragma unroll
-                for (int j = 0; j < kB; ++j)
-                    if (yb + j < y1) w[j] = __ldcg(from + (size_t)(yb + j) * g.WW + x);
-#pragma unroll
-                for (int j = 0; j < kB; ++j)
-                    if (yb + j < y1) to[pidx(g, yb + j, x)] = w[j];
-            }
-        });
-    };
-    copy_in(src, g.I);
-    if (with_xs) copy_in(src + wimg, g.XS);
-    if (p.keep) pack_plane(p.keep + pix, g.K, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
-    if (p.avoid) pack_plane(p.avoid + pix, g.A, g, p.err, ERR_CONSTRAINT_NOT_BINARY);
+    const uint32_t *src = p.xbuf + (size_t)img * 4 * wimg;
+    load_rows(g, src, g.I);
+    if (with_xs) load_rows(g, src + wimg, g.XS);
+    (void)pix;
+    if (p.packed_io) {
+        if (p.keep) load_rows(g, reinterpret_cast<const uint32_t *>(p.keep) + (size_t)img * wimg, g.K);
+        if (p.avoid) load_rows(g, reinterpret_cast<const uint32_t *>(p.avoid) + (size_t)img * wimg, g.A);
+    } else {   // packed by the image's first segment (store_state_nl)
+        if (p.keep) load_rows(g, src + 2 * wimg, g.K);
+        if (p.avoid) load_rows(g, src + 3 * wimg, g.A);
+    }
 }
 
 // segment epilogue: the bit-plane to xbuf for the next segment (L2)
 template <bool HOT>
-__device__ __noinline__ void store_state_nl(const View &v, uint32_t *dst, bool with_xs) {
+__device__ __noinline__ void store_state_nl(const View &v, uint32_t *dst, bool with_xs, bool with_k, bool with_a) {
     const Img g = make_img<HOT>(v);
     const size_t wimg = (size_t)g.H * g.WW;
+    // slots: 0 the image, 1 XS, 2 / 3 keep / avoid packed once (first segment)
     for_strip(g, [&](int y, int x, int q) {
-        __stcg(dst + (size_t)y * g.WW + x, g.I[q]);
-        if (with_xs) __stcg(dst + wimg + (size_t)y * g.WW + x, g.XS[q]);
+        const size_t o = (size_t)y * g.WW + x;
+        __stcg(dst + o, g.I[q]);
+        if (with_xs) __stcg(dst + wimg + o, g.XS[q]);
+        if (with_k) __stcg(dst + 2 * wimg + o, g.K[q]);
+        if (with_a) __stcg(dst + 3 * wimg + o, g.A[q]);
     });
 }
 
@@ -2144,7 +2159,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             store_image_nl<HOT>(v, p.out + pix,
                                 p.packed_io ? reinterpret_cast<uint32_t *>(p.out) + (size_t)img * p.H * p.WW : nullptr);
         else
-            store_state_nl<HOT>(v, p.xbuf + (size_t)img * 2 * p.H * p.WW, reads_xs(first + k1 % nst));
+            store_state_nl<HOT>(v, p.xbuf + (size_t)img * 4 * p.H * p.WW, reads_xs(first + k1 % nst),
+                                seg == 0 && has_k && !p.packed_io, seg == 0 && has_a && !p.packed_io);
         stamp(5);
         if (lead && p.stats) {   // accumulated over the image's segments (zeroed buffer)
             unsigned long long *sp = reinterpret_cast<unsigned long long *>(p.stats + (size_t)img * kStatFields);

@@ -116,7 +116,7 @@ struct KParams {
     unsigned *done;
     int chunk;
     int fused;              // 1: fused prep + E-pass allowed (the planner left out the R planes)
-    int packed_io;          // 1: in / out are [n][H][WW] uint32 bit rows (host-packed, validated)
+    int packed_io;          // 1: in / out (and keep / avoid) are [n][H][WW] uint32 bit rows (binary by construction)
     // segmented scheduling (batches larger than one wave, single-CTA images):
     // an image's stage list is cut into nseg segments (see seg_range);
     // the queue hands out (segment, image) tasks segment-major, the image's
@@ -125,7 +125,7 @@ struct KParams {
     // predecessor).  nseg == 1: whole images.
     int nseg;
     int seg_stages, seg_fine;   // segments of seg_stages stages, the last seg_fine stages one each
-    uint32_t *xbuf;         // [n][2][H][WW]: the image, and XS when the next stage reads it
+    uint32_t *xbuf;         // [n][4][H][WW]: the image, XS when the next stage reads it, keep, avoid
     unsigned *progress;
     long long *trace;       // debug: per task kTraceFields int64 (see hasf_kernel) or null
     long long trace_cap;    // tasks recorded

@@ -32,6 +32,7 @@ class Config:
     rad_lo: float = 8.0
     rad_hi: float = 60.0
     noise: float = 0.05
+    constraints: float = 0.0   # > 0: seeded keep / avoid masks (constraint_masks), SURVEY §8 row f4
 
 
 CONFIGS = {
@@ -40,6 +41,9 @@ CONFIGS = {
     "c2": Config("c2", 32, 2048, 2048, 10, 8, 2000, "blobs", 160, 30, 240, 0.10),
     "c3": Config("c3", 1, 8192, 8192, 8, 8, 3000, "blobs", 2000, 10, 400, 0.05),
     "c4": Config("c4", 1024, 256, 256, 4, 4, 4000, "mazes", 0, 0, 0, 0.02),
+    # c1 with control images (reference smoothing.py:197-206): 1% of the object
+    # pixels must stay object (keep), 1% of the background must stay background
+    "c1k": Config("c1k", 256, 512, 512, 5, 8, 1000, "blobs", 40, 8, 60, 0.05, 0.01),
 }
 
 
@@ -161,6 +165,24 @@ def config_batch(cfg: Config | str, start: int = 0, count: int | None = None) ->
     for k in range(count):
         out[k] = config_image(cfg, start + k)
     return out
+
+
+def constraint_masks(cfg: Config | str, imgs: np.ndarray, start: int = 0):
+    """Seeded keep / avoid masks for a batch of config images (image i uses
+    seed base_seed + start + i + 500000): keep = each object pixel with
+    probability cfg.constraints, avoid = each background pixel likewise.
+    Disjoint, keep inside the object, avoid outside it (the reference's
+    validity conditions, smoothing.py:199-206)."""
+    cfg = CONFIGS[cfg] if isinstance(cfg, str) else cfg
+    frac = cfg.constraints or 0.01
+    keep = np.empty_like(imgs)
+    avoid = np.empty_like(imgs)
+    for k in range(len(imgs)):
+        rng = np.random.default_rng(cfg.base_seed + start + k + 500000)
+        u = rng.random(imgs[k].shape)
+        keep[k] = (imgs[k] == 1) & (u < frac)
+        avoid[k] = (imgs[k] == 0) & (u < frac)
+    return keep, avoid
 
 
 def jagged_disc(h, w, radius, amplitudes=((9, 12.0, 0.0), (23, 7.0, 1.2), (41, 4.0, 0.3))):

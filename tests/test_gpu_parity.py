@@ -543,3 +543,35 @@ def test_cli_smooth_and_benchmark_on_device(tmp_path, capsys):
     lines = capsys.readouterr().out.strip().splitlines()
     assert lines[0] == "scheduler,workers,t_min_s,speedup,efficiency" and len(lines) == 3
     assert lines[1].startswith("nps,1,")
+
+
+def test_constrained_hasf_at_scale_c1k():
+    """Row f4: constrained HASF (keep / avoid control images, reference
+    smoothing.py:197-206) on 16 full-size c1k images vs the oracle, in a
+    batch larger than one wave (segmented) and through the streamed host
+    entry with bit-packed constraint planes."""
+    cfg = W.CONFIGS["c1k"]
+    imgs = W.config_batch(cfg, 0, 300)
+    keep, avoid = W.constraint_masks(cfg, imgs)
+    got = P.hasf_batch(torch.from_numpy(imgs).cuda(), cfg.r_max, P.ADJ_84, keep=torch.from_numpy(keep).cuda(),
+                       avoid=torch.from_numpy(avoid).cuda()).cpu().numpy()
+    sel = list(range(8)) + list(range(292, 300))
+    want = O.hasf_batch(imgs[sel], cfg.r_max, 8, keep=keep[sel], avoid=avoid[sel], threads=16)
+    assert np.array_equal(got[sel], want)
+    assert np.all(got[keep == 1] == 1) and np.all(got[avoid == 1] == 0)
+    lib = _lib.load()
+    n = 40
+    out = np.zeros_like(imgs[:n])
+    _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, n, cfg.h, cfg.w, cfg.r_max, 8,
+                                      keep.ctypes.data, avoid.ctypes.data, torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(out, got[:n])
+    bad = keep[:n].copy()
+    bad[33, 0, 0], bad[33, 0, 1] = 1, 2   # a non-binary constraint pixel in a late chunk
+    rc = lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, n, cfg.h, cfg.w, cfg.r_max, 8, bad.ctypes.data,
+                                avoid.ctypes.data, torch.cuda.current_stream().cuda_stream)
+    assert rc == _lib.TS_ERR_VALUE and b"0 or 1" in lib.ts_last_error()
+    k2 = keep[:n].copy()
+    k2[5] |= (imgs[5] == 0)   # keep outside the object: the device-side check
+    rc = lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, n, cfg.h, cfg.w, cfg.r_max, 8, k2.ctypes.data,
+                                None, torch.cuda.current_stream().cuda_stream)
+    assert rc == _lib.TS_ERR_VALUE and b"keep-constraint pixels must be object pixels" in lib.ts_last_error()
