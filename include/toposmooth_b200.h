@@ -138,6 +138,16 @@ int64_t ts_set_smem_budget(int64_t bytes);
  * previous value. */
 int32_t ts_set_dense_divisor(int32_t div);
 
+/* Non-blocking ts_hasf_batch for device-resident callers: stream-ordered, no
+ * synchronization inside; the device-side error code (0 = none) is written to
+ * the caller's device int *err_dev in stream order (zeroed by the call).
+ * Returns host-side argument / launch errors only.  Map a code read back
+ * later with ts_check_device_error (status + ts_last_error message). */
+int ts_hasf_batch_async(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                        int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev, void *stream,
+                        int32_t *err_dev);
+int ts_check_device_error(int32_t code);
+
 /* ---- netpbm P4 straight to / from the device bit-row layout -------------
  * P4 rasters (reference netpbm.py:68-129, the raster bytes after the header):
  * [n][h][(w + 7) / 8] bytes, 1 bit per pixel, MSB first, rows padded to a

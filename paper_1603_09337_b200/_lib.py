@@ -29,6 +29,8 @@ SIGNATURES = {
     "ts_max_radius": ([], ctypes.c_int),
     "ts_hasf_batch": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp], ctypes.c_int),
     "ts_hasf_batch_host": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp], ctypes.c_int),
+    "ts_hasf_batch_async": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "ts_check_device_error": ([_i32], ctypes.c_int),
     "ts_cutting_batch": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "ts_filling_batch": ([_vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "ts_thin_batch": ([_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i64, _vp], ctypes.c_int),

@@ -194,27 +194,40 @@ int plan_strips(int H, int WW, int threads, Plan &pl) {
     return best_cost;
 }
 
-// Keep freed workspace in the device's stream-ordered pool across calls (the
-// default release threshold of 0 returns it to the OS at every synchronize,
-// which re-maps tens of MB per call).  Once per device.
+// Workspace comes from a PRIVATE stream-ordered memory pool per device whose
+// release threshold keeps freed blocks cached across calls (the default
+// threshold of 0 would return them to the OS at every synchronize and
+// re-map tens of MB per call).  The device's default pool -- shared with
+// the rest of the process -- is left untouched.
 std::mutex g_pool_mu;
-bool g_pool_done[64] = {};
+cudaMemPool_t g_pool[64] = {};
 
-void retain_pool(int dev) {
-    std::lock_guard<std::mutex> lk(g_pool_mu);
-    if (dev < 0 || dev >= 64 || g_pool_done[dev]) return;
+cudaError_t ws_malloc(void **ptr, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.handleTypes = cudaMemHandleTypeNone;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if ((e = cudaMemPoolCreate(&g_pool[dev], &props)) != cudaSuccess) return e;
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool = g_pool[dev];
     }
-    g_pool_done[dev] = true;
+    return cudaMallocFromPoolAsync(ptr, bytes, pool, st);
 }
 
 int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
     int dev = 0;
     TS_CUDA(cudaGetDevice(&dev));
-    retain_pool(dev);
     TS_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
     TS_CUDA(cudaDeviceGetAttribute(smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     TS_CUDA(cudaDeviceGetAttribute(smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
@@ -436,12 +449,12 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     if (team_out) *team_out = team;
     char *ctrl = nullptr;
     uint32_t *gws = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&ctrl, ctrl_bytes, st));
+    TS_CUDA(ws_malloc((void **)&ctrl, ctrl_bytes, st));
     if (ws_words + xbuf_words) {
-        cudaError_t e = cudaMallocAsync((void **)&gws, (ws_words + xbuf_words) * 4, st);
+        cudaError_t e = ws_malloc((void **)&gws, (ws_words + xbuf_words) * 4, st);
         if (e != cudaSuccess) {
             cudaFreeAsync(ctrl, st);
-            return cuda_fail(e, "cudaMallocAsync(workspace)");
+            return cuda_fail(e, "ws_malloc(workspace)");
         }
     }
     TS_CUDA(cudaMemsetAsync(ctrl, 0, ctrl_bytes, st));
@@ -519,7 +532,7 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     if (n <= 0) return fused_launch(mode, in, out, n, h, w, r_first, r_last, do_cut, do_fill, fg, keep, avoid, prio,
                                     max_sweeps, st, stats_host, nullptr, nullptr) ?: ok();
     int *err = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), st));
+    TS_CUDA(ws_malloc((void **)&err, sizeof(int), st));
     cudaError_t me = cudaMemsetAsync(err, 0, sizeof(int), st);
     int rc = me == cudaSuccess ? fused_launch(mode, in, out, n, h, w, r_first, r_last, do_cut, do_fill, fg, keep,
                                               avoid, prio, max_sweeps, st, stats_host, err, nullptr)
@@ -577,6 +590,26 @@ int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
     if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
     return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr, -1,
                      (cudaStream_t)stream, stats_host);
+}
+
+// Non-blocking variant for callers whose buffers already live on the device:
+// everything is stream-ordered, nothing synchronizes; the device error code
+// (0 = none) lands in *err_dev in stream order -- read it whenever convenient
+// and map it with ts_check_device_error.
+int ts_hasf_batch_async(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r_max,
+                        int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev, void *stream,
+                        int32_t *err_dev) {
+    if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
+    if (!err_dev) return fail(TS_ERR_VALUE, "err_dev is required");
+    cudaStream_t st = (cudaStream_t)stream;
+    TS_CUDA(cudaMemsetAsync(err_dev, 0, sizeof(int32_t), st));
+    return fused_launch(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr, -1, st,
+                        nullptr, reinterpret_cast<int *>(err_dev), nullptr) ?: ok();
+}
+
+int ts_check_device_error(int32_t code) {
+    if (code == 0) return ok();
+    return device_error(code, MODE_HASF);
 }
 
 // ---- streamed host entry ---------------------------------------------------
@@ -664,8 +697,8 @@ int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     uint8_t *d = nullptr;
     int *err = nullptr;
     unsigned *flags = nullptr;   // ready[nchunks], done[nchunks]
-    TS_CUDA(cudaMallocAsync((void **)&d, bytes * nbuf, user));
-    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
+    TS_CUDA(ws_malloc((void **)&d, bytes * nbuf, user));
+    TS_CUDA(ws_malloc((void **)&err, sizeof(int), user));
     int dev = 0;
     TS_CUDA(cudaGetDevice(&dev));
     flags = take_flags(dev);
@@ -712,6 +745,8 @@ int hasf_host_streamed(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     cudaEventRecord(eo, sout);
     cudaStreamWaitEvent(user, ec, 0);
     cudaStreamWaitEvent(user, eo, 0);
+    cudaEventRecord(ev0, sin);   // ev0 reused: the copy-in stream drained too (also on error paths)
+    cudaStreamWaitEvent(user, ev0, 0);
     int herr = 0;
     cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, user);
     const std::string keep_msg = g_err;
@@ -754,7 +789,7 @@ struct Stage {
 struct HostCtx {
     bool made = false;
     cudaStream_t sin = nullptr, sout = nullptr, sc = nullptr;
-    cudaEvent_t ev0 = nullptr, ec = nullptr;
+    cudaEvent_t ev0 = nullptr, ec = nullptr, ein = nullptr;
     cudaEvent_t eo[kMaxChunks] = {};
 };
 HostCtx g_ctx[64];
@@ -768,6 +803,7 @@ int host_ctx(int dev, HostCtx *&c) {
     TS_CUDA(cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking));
     TS_CUDA(cudaEventCreateWithFlags(&c->ev0, cudaEventDisableTiming));
     TS_CUDA(cudaEventCreateWithFlags(&c->ec, cudaEventDisableTiming));
+    TS_CUDA(cudaEventCreateWithFlags(&c->ein, cudaEventDisableTiming));
     for (int k = 0; k < kMaxChunks; ++k) TS_CUDA(cudaEventCreateWithFlags(&c->eo[k], cudaEventDisableTiming));
     c->made = true;
     return TS_OK;
@@ -814,8 +850,8 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
     if ((rc = host_ctx(dev, hc))) return rc;
     uint32_t *d = nullptr;
     int *err = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&d, words * 4 * 4, user));
-    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
+    TS_CUDA(ws_malloc((void **)&d, words * 4 * 4, user));
+    TS_CUDA(ws_malloc((void **)&err, sizeof(int), user));
     TS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), user));
     unsigned *flags = take_flags(dev);
     if (!flags) return fail(TS_ERR_CUDA, "cudaMalloc(chunk flags)");
@@ -849,19 +885,22 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
                           (int)chunk, 1);
     const bool launched = e == cudaSuccess && mrc == 0 && rc == TS_OK;
     if (launched) {
+        // the rest of the input: pack chunk k while chunk k-1 is on the link
+        // (after a bad chunk the flags are still raised so the launch drains).
+        // Every send is enqueued before any copy-back wait: were the streams'
+        // work funnelled into one hardware queue, a wait ahead of a send
+        // would block the copy the kernel is waiting for.
+        for (int k = 1; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
+            const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
+            if (!bad && !pack_chunk(i0, cnt)) bad = true;
+            send(k);
+        }
         for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
             const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
             mrc = mo.wait(sout, (unsigned long long)(uintptr_t)(done + k), (unsigned)cnt, kWaitGeq);
             if (mrc == 0)
                 e = cudaMemcpyAsync(hout + i0 * wimg, dout + i0 * wimg, cnt * wimg * 4, cudaMemcpyDeviceToHost, sout);
             if (e == cudaSuccess) e = cudaEventRecord(eo[k], sout);
-        }
-        // the rest of the input: pack chunk k while chunk k-1 is on the link
-        // (after a bad chunk the flags are still raised so the launch drains)
-        for (int k = 1; k < nchunks && e == cudaSuccess && mrc == 0; ++k) {
-            const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
-            if (!bad && !pack_chunk(i0, cnt)) bad = true;
-            send(k);
         }
         // results: unpack chunk k as soon as its copy-back finished
         for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0 && !bad; ++k) {
@@ -870,8 +909,13 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
             if (e == cudaSuccess) unpack_images(hout + i0 * wimg, out_host + i0 * img, cnt, h, w, ww);
         }
     }
+    // the user stream (which frees the buffers) waits for all three streams,
+    // on every exit path -- also the copy-in stream, whose copies may still
+    // target the buffers when the launch failed
     cudaEventRecord(ec, sc);
     cudaStreamWaitEvent(user, ec, 0);
+    cudaEventRecord(hc->ein, sin);
+    cudaStreamWaitEvent(user, hc->ein, 0);
     if (launched) {
         cudaEvent_t el = eo[nchunks - 1];
         if (el) cudaStreamWaitEvent(user, el, 0);
@@ -936,9 +980,13 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     // nsys) or CUDA_LAUNCH_BLOCKING, where it would only time out
     static const bool serialised = [] {
         const char *lb = getenv("CUDA_LAUNCH_BLOCKING");
+        // fewer hardware queues than the entry's three streams (copy-in,
+        // kernel, copy-out) may serialise a copy behind the kernel that waits for it
+        const char *mc = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+        const bool few_queues = mc && atoi(mc) > 0 && atoi(mc) < 3;
         return getenv("CUDA_INJECTION64_PATH") != nullptr || getenv("NV_TPS_LAUNCH_TOKEN") != nullptr ||
                getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr ||
-               getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr || (lb && lb[0] == '1');
+               getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr || (lb && lb[0] == '1') || few_queues;
     }();
     if (!big && !serialised && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR) {
         if (g_streamed.load() == 1)
@@ -951,8 +999,8 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     uint8_t *d = nullptr;
     int *err = nullptr;
     const int nbuf = 2 + (keep_host ? 1 : 0) + (avoid_host ? 1 : 0);
-    TS_CUDA(cudaMallocAsync((void **)&d, bytes * nbuf, user));
-    TS_CUDA(cudaMallocAsync((void **)&err, sizeof(int), user));
+    TS_CUDA(ws_malloc((void **)&d, bytes * nbuf, user));
+    TS_CUDA(ws_malloc((void **)&err, sizeof(int), user));
     TS_CUDA(cudaMemsetAsync(err, 0, sizeof(int), user));
     uint8_t *din = d, *dout = d + bytes;
     uint8_t *dk = keep_host ? d + 2 * bytes : nullptr;
@@ -1060,7 +1108,7 @@ static int run_edt(const uint8_t *in, const int64_t *g_in, void *out, int64_t n,
         TS_CUDA(cudaStreamSynchronize(st));
         return ok();
     }
-    TS_CUDA(cudaMallocAsync((void **)&stk, sizeof(long long) * (px * 2 + (g_in ? 0 : px)), st));
+    TS_CUDA(ws_malloc((void **)&stk, sizeof(long long) * (px * 2 + (g_in ? 0 : px)), st));
     g = g_in ? const_cast<long long *>(reinterpret_cast<const long long *>(g_in)) : stk + 2 * px;
     cudaError_t e = cudaSuccess;
     if (!g_in) e = launch_edt_phase1(in, g, (int)n, h, w, invert, inf, st);
@@ -1116,7 +1164,7 @@ int ts_simple_point_mask_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t 
     if (n == 0) return ok();
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *dlut = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&dlut, 256, st));
+    TS_CUDA(ws_malloc((void **)&dlut, 256, st));
     const uint8_t *src = fg == 8 ? tables().s84 : tables().s48;
     cudaError_t e = cudaMemcpyAsync(dlut, src, 256, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = launch_classify(in_dev, out_dev, (int)n, h, w, dlut, st);
@@ -1137,8 +1185,8 @@ int ts_component_counts_batch(const uint8_t *in_dev, int64_t *counts_host, int64
     cudaStream_t st = (cudaStream_t)stream;
     int *parent = nullptr;
     long long *cnt = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&parent, sizeof(int) * (size_t)n * ((size_t)h * w + 1), st));
-    TS_CUDA(cudaMallocAsync((void **)&cnt, sizeof(long long) * (size_t)n, st));
+    TS_CUDA(ws_malloc((void **)&parent, sizeof(int) * (size_t)n * ((size_t)h * w + 1), st));
+    TS_CUDA(ws_malloc((void **)&cnt, sizeof(long long) * (size_t)n, st));
     cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(long long) * (size_t)n, st);
     if (e == cudaSuccess)
         e = launch_ccl(in_dev, parent, cnt, (int)n, h, w, conn, foreground ? 1 : 0, exterior ? 1 : 0, st);
@@ -1182,7 +1230,7 @@ int ts_hasf_batch_p4(const uint8_t *p4_in_dev, uint8_t *p4_out_dev, int64_t n, i
     const int ww = (w + 31) / 32;
     const size_t words = (size_t)n * h * ww;
     char *ws = nullptr;
-    TS_CUDA(cudaMallocAsync((void **)&ws, 4 * words * 4 + 64, st));
+    TS_CUDA(ws_malloc((void **)&ws, 4 * words * 4 + 64, st));
     uint32_t *rin = reinterpret_cast<uint32_t *>(ws), *rout = rin + words, *rk = rout + words, *ra = rk + words;
     int *err = reinterpret_cast<int *>(ra + words);
     cudaError_t e = cudaMemsetAsync(err, 0, sizeof(int), st);

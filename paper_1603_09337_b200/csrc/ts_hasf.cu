@@ -2,6 +2,7 @@
 // ts_hasf_impl.cuh; one translation unit per <adjacency, placement, threads>
 // variant).
 #include <cuda_runtime.h>
+#include <mutex>
 #include "ts_internal.h"
 
 namespace ts {
@@ -15,6 +16,22 @@ TS_DECLARE_HASF_VARIANT(4h)
 TS_DECLARE_HASF_VARIANT(4g)
 TS_DECLARE_HASF_VARIANT(8h256)
 TS_DECLARE_HASF_VARIANT(4h256)
+
+cudaError_t raise_smem_limit_once(const void *fn, std::mutex &mu, bool (&done)[64]) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev]) return cudaSuccess;
+    int optin = 0;
+    cudaFuncAttributes fa{};
+    if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+    if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) done[dev] = true;
+    return e;
+}
 
 // threads: 512 (any placement) or 256 (hot placement only, two CTAs per SM)
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream) {

@@ -54,6 +54,7 @@
 // reference from shared memory (a by-value View cost 15% in ABI copies).
 #pragma once
 #include <cuda_runtime.h>
+#include <mutex>
 #include "ts_common.cuh"
 #include "ts_internal.h"
 
@@ -2207,11 +2208,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
 // per-variant host entry points, one translation unit each (ts_hasf_<fg><h|g>.cu)
 }  // namespace TS_IMPL_NS
 
+// The kernel's dynamic shared-memory limit is a process-wide function
+// attribute: it is raised ONCE per device to the opt-in maximum (never changed
+// per call, so concurrent host threads planning different images cannot race
+// a launch against a smaller limit).
+cudaError_t raise_smem_limit_once(const void *fn, std::mutex &mu, bool (&done)[64]);
+
 #define TS_DEFINE_HASF_VARIANT(FG, HOT, SUFFIX)                                                                \
+    static std::mutex g_attr_mu_##SUFFIX;                                                                      \
+    static bool g_attr_done_##SUFFIX[64];                                                                      \
     cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream) {      \
         using namespace TS_IMPL_NS;                                                                             \
         const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
+        cudaError_t e = raise_smem_limit_once(fn, g_attr_mu_##SUFFIX, g_attr_done_##SUFFIX);                   \
         if (e != cudaSuccess) return e;                                                                         \
         void *args[] = {(void *)&p};                                                                            \
         if (p.team > 1)                                                                                         \
@@ -2221,7 +2230,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks) {                                       \
         using namespace TS_IMPL_NS;                                                                             \
         const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
+        cudaError_t e = raise_smem_limit_once(fn, g_attr_mu_##SUFFIX, g_attr_done_##SUFFIX);                   \
         if (e != cudaSuccess) return e;                                                                         \
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, kThreads, smem_bytes);                \
     }

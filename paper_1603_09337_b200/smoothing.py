@@ -108,7 +108,20 @@ def smooth(img, r_max: int, workers: int = 1, scheduler: str = "nps") -> np.ndar
     return hasf(img, SmoothingConfig(r_max=r_max, workers=workers, scheduler=scheduler))
 
 
-def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=None, stats: bool = False):
+class PendingCheck:
+    """Device error flag of a non-blocking hasf_batch (ts_hasf_batch_async):
+    check() waits for the flag (a 4-byte read in stream order) and raises the
+    reference's exception classes like the blocking call."""
+
+    def __init__(self, err):
+        self.err = err
+
+    def check(self) -> None:
+        check(load().ts_check_device_error(int(self.err.item())))
+
+
+def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=None, stats: bool = False,
+               blocking: bool = True):
     """HASF on every image of an [n, h, w] batch in one launch.
 
     torch CUDA tensors stay on the device (returns a CUDA uint8 tensor); numpy
@@ -117,6 +130,9 @@ def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=Non
     returns an int64 [n, 16] array: sweeps, fixpoint passes, engine calls, flips,
     cycles in prep / fixpoint passes / apply+re-examination / total, then
     tiny-sweep and dense-sweep breakdowns (see csrc/ts_internal.h kStatFields).
+    With blocking=False (CUDA tensors only, no stats) nothing synchronizes:
+    returns (out, PendingCheck); out is valid in stream order and
+    PendingCheck.check() raises any device-side validation error.
     """
     import torch
     r_max = _check_radius(r_max)
@@ -131,6 +147,13 @@ def hasf_batch(images, r_max: int, adj: Adjacency = ADJ_84, keep=None, avoid=Non
         if t is not None and tuple(t.shape) != (n, h, w):
             raise ValueError(f"{name} constraint shape {tuple(t.shape)} != batch shape {(n, h, w)}")
     out = torch.empty_like(x)
+    if not blocking:
+        if is_numpy or stats:
+            raise ValueError("blocking=False needs CUDA tensor input and stats=False")
+        err = torch.zeros(1, dtype=torch.int32, device=x.device)
+        check(load().ts_hasf_batch_async(x.data_ptr(), out.data_ptr(), n, h, w, r_max, adj.fg, D.ptr(k), D.ptr(a),
+                                         D.stream_ptr(), err.data_ptr()))
+        return out, PendingCheck(err)
     st = np.zeros((n, 36), np.int64) if stats else None
     check(load().ts_hasf_batch(x.data_ptr(), out.data_ptr(), n, h, w, r_max, adj.fg, D.ptr(k), D.ptr(a),
                                D.stream_ptr(), None if st is None else st.ctypes.data))

@@ -67,3 +67,14 @@ def test_two_rank_gloo_batch():
     for rank, out, t in res:
         assert np.array_equal(out, want), rank
         assert t == 11.0
+
+
+def test_pack_rows_is_p4_layout():
+    import torch
+    from paper_1603_09337_b200.dist import pack_rows, unpack_rows
+    rng = np.random.default_rng(9)
+    for w in (1, 7, 8, 13, 40):
+        a = (rng.random((3, 4, w)) < 0.5).astype(np.uint8)
+        p = pack_rows(torch.from_numpy(a))
+        assert np.array_equal(p.numpy(), np.packbits(a, axis=2))
+        assert np.array_equal(unpack_rows(p, w).numpy(), a)

@@ -575,3 +575,26 @@ def test_constrained_hasf_at_scale_c1k():
     rc = lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, n, cfg.h, cfg.w, cfg.r_max, 8, k2.ctypes.data,
                                 None, torch.cuda.current_stream().cuda_stream)
     assert rc == _lib.TS_ERR_VALUE and b"keep-constraint pixels must be object pixels" in lib.ts_last_error()
+
+
+def test_nonblocking_batch_and_library_hygiene():
+    """blocking=False: no synchronization inside, errors surface through the
+    pending check; the device's default memory pool is left untouched (the
+    library keeps a private pool)."""
+    imgs = torch.from_numpy(W.config_batch("c4", 4500, 6)).cuda()
+    out, pending = P.hasf_batch(imgs, 4, P.ADJ_48, blocking=False)
+    pending.check()
+    assert torch.equal(out, P.hasf_batch(imgs, 4, P.ADJ_48))
+    bad = imgs.clone()
+    bad[3, 7, 7] = 5
+    out, pending = P.hasf_batch(bad, 4, P.ADJ_48, blocking=False)
+    with pytest.raises(ValueError, match="0 or 1"):
+        pending.check()
+    import ctypes
+    cudart = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    if cudart is not None:
+        pool_h = ctypes.c_void_p()
+        assert cudart.cudaDeviceGetDefaultMemPool(ctypes.byref(pool_h), 0) == 0
+        thr = ctypes.c_uint64()
+        assert cudart.cudaMemPoolGetAttribute(pool_h, 4, ctypes.byref(thr)) == 0   # ReleaseThreshold
+        assert thr.value == 0
