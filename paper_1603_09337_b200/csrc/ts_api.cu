@@ -27,8 +27,8 @@ cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, c
 cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm);
 cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
                               cudaStream_t st);
-cudaError_t launch_edt_phase2(const long long *g, void *out, long long *stk, int n, int H, int W, long long inf,
-                              int out_mode, long long thr, cudaStream_t st);
+cudaError_t launch_edt(const uint8_t *pix, const long long *g64, void *out, int *scratch, int n, int H, int W,
+                       int invert, long long inf, int out_mode, long long thr, cudaStream_t st);
 cudaError_t launch_classify(const uint8_t *pix, uint8_t *out, int n, int H, int W, const uint8_t *lut,
                             cudaStream_t st);
 cudaError_t launch_selftest_circuit(uint8_t *out84, uint8_t *out48, cudaStream_t st);
@@ -1102,18 +1102,16 @@ static int run_edt(const uint8_t *in, const int64_t *g_in, void *out, int64_t n,
     if (n == 0) return ok();
     const long long inf = (long long)h * h + (long long)w * w + 1;   // edt.py:25-28
     const size_t px = (size_t)n * h * w;
-    long long *g = nullptr, *stk = nullptr;
     if (phase1_only) {
         TS_CUDA(launch_edt_phase1(in, reinterpret_cast<long long *>(out), (int)n, h, w, invert, inf, st));
         TS_CUDA(cudaStreamSynchronize(st));
         return ok();
     }
-    TS_CUDA(ws_malloc((void **)&stk, sizeof(long long) * (px * 2 + (g_in ? 0 : px)), st));
-    g = g_in ? const_cast<long long *>(reinterpret_cast<const long long *>(g_in)) : stk + 2 * px;
-    cudaError_t e = cudaSuccess;
-    if (!g_in) e = launch_edt_phase1(in, g, (int)n, h, w, invert, inf, st);
-    if (e == cudaSuccess) e = launch_edt_phase2(g, out, stk, (int)n, h, w, inf, out_mode, thr, st);
-    cudaFreeAsync(stk, st);
+    int *scratch = nullptr;
+    TS_CUDA(ws_malloc((void **)&scratch, sizeof(int) * px * 4, st));
+    cudaError_t e = launch_edt(in, reinterpret_cast<const long long *>(g_in), out, scratch, (int)n, h, w, invert, inf,
+                               out_mode, thr, st);
+    cudaFreeAsync(scratch, st);
     cudaError_t se = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "edt launch");
     if (se != cudaSuccess) return cuda_fail(se, "edt kernels");

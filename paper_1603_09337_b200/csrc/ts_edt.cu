@@ -2,13 +2,20 @@
 // kernels for sm_100a.  These back the stage-level parity API (edt_squared,
 // edt_phase1_columns, edt_phase2_rows, background_distances, dilate, erode,
 // neighborhood_codes, simple_point_mask); the fused HASF kernel uses its own
-// radius-clamped bit-parallel EDT (ts_hasf.cu).
+// radius-clamped bit-parallel EDT (ts_hasf_impl.cuh).
 //
-// Phase 1 (edt.py:45-71): one thread per column, down then up sweep; adjacent
-// threads touch adjacent columns, so every row step is one coalesced access.
-// Phase 2 (edt.py:74-119): one thread per row builds the lower envelope of the
-// parabolas (x-u)^2 + g(u)^2; its stacks s,t live in a column-major scratch
-// ([W][rows]) so that the 32 rows of a warp hit consecutive addresses.
+// All arithmetic is int32 (g^2 + u^2 <= 2 * 32767^2 < 2^31, and
+// INF = h^2 + w^2 + 1 fits); int64 appears only at the API (the reference's
+// dtype).  Every global access is coalesced:
+//   phase 1 (edt.py:45-71): one thread per column, down then up sweep; a
+//     warp's 32 columns are adjacent, so each row step is one transaction;
+//   transpose: 32x32 shared-memory tiles, g [H][W] -> gT [W][H];
+//   phase 2 (edt.py:74-119): one thread per ROW on the transposed map -- the
+//     32 rows of a warp read gT[u][row..row+31] together, and the lower-
+//     envelope stacks s, t live as [q][row] for the same reason; the result
+//     goes out transposed (outT [W][H]);
+//   transpose back, fused with the output conversion (int64 distance, border
+//     term of morph.py:25-31, dilate / erode thresholds).
 #include <cuda_runtime.h>
 #include <cstdint>
 #include "ts_common.cuh"
@@ -22,110 +29,128 @@ __device__ __forceinline__ long long floordiv_pos(long long a, long long b) {
     return q;
 }
 
-__global__ void edt_phase1_kernel(const uint8_t *__restrict__ pix, long long *__restrict__ g, int n, int H, int W,
-                                  int invert, long long inf) {
+template <class T>
+__global__ void edt_phase1_kernel(const uint8_t *__restrict__ pix, T *__restrict__ g, int n, int H, int W, int invert,
+                                  int inf) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
     if (c >= W || b >= n) return;
     const uint8_t *p = pix + (size_t)b * H * W + c;
-    long long *gg = g + (size_t)b * H * W + c;
-    long long prev = (p[0] != invert) ? 0 : inf;
+    T *gg = g + (size_t)b * H * W + c;
+    int prev = (p[0] != invert) ? 0 : inf;
     gg[0] = prev;
     for (int r = 1; r < H; ++r) {
-        long long v;
-        if (p[(size_t)r * W] != invert)
-            v = 0;
-        else
-            v = prev < inf ? prev + 1 : inf;
+        const int v = p[(size_t)r * W] != invert ? 0 : (prev < inf ? prev + 1 : inf);
         gg[(size_t)r * W] = v;
         prev = v;
     }
     for (int r = H - 2; r >= 0; --r) {
-        const long long cur = gg[(size_t)r * W];
+        const int cur = (int)gg[(size_t)r * W];
         if (prev < cur) {
-            const long long v = prev + 1;
-            gg[(size_t)r * W] = v;
-            prev = v;
+            gg[(size_t)r * W] = ++prev;
         } else {
             prev = cur;
         }
     }
 }
 
-// out_mode: 0 -> int64 distance; 1 -> int64 min(distance, border^2)
-//           2 -> uint8 (distance <= thr)      3 -> uint8 (min(distance, border^2) > thr)
-__global__ void edt_phase2_kernel(const long long *__restrict__ g, void *__restrict__ out, long long *__restrict__ stk,
-                                  int n, int H, int W, long long inf, int out_mode, long long thr) {
+// [n][H][W] (TI) -> [n][W][H] int32, 32x32 tiles through shared memory
+template <class TI>
+__global__ void transpose_in_kernel(const TI *__restrict__ src, int *__restrict__ dst, int H, int W) {
+    __shared__ int tile[32][33];
+    const size_t img = (size_t)blockIdx.z * H * W;
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int y = y0 + j, x = x0 + threadIdx.x;
+        if (y < H && x < W) tile[j][threadIdx.x] = (int)src[img + (size_t)y * W + x];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int x = x0 + j, y = y0 + threadIdx.x;
+        if (y < H && x < W) dst[img + (size_t)x * H + y] = tile[threadIdx.x][j];
+    }
+}
+
+// lower envelope of the parabolas (x-u)^2 + g(u)^2 of one row (edt.py:74-119),
+// on the transposed map: gT[u * H + row], stacks s/t at [q * H + row]
+__global__ void edt_phase2T_kernel(const int *__restrict__ gT, int *__restrict__ outT, int *__restrict__ stk, int n,
+                                   int H, int W, int inf) {
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
     if (row >= H || b >= n) return;
-    const long long *gr = g + ((size_t)b * H + row) * W;
-    const size_t rows_total = (size_t)n * H;
-    const size_t myrow = (size_t)b * H + row;
-    // column-major stacks: s at stk[u * rows_total + myrow], t after W*rows_total
-    long long *S = stk + myrow;
-    long long *T = stk + (size_t)W * rows_total + myrow;
-    auto s_at = [&](long long q) -> long long & { return S[(size_t)q * rows_total]; };
-    auto t_at = [&](long long q) -> long long & { return T[(size_t)q * rows_total]; };
-    long long q = -1;
-    for (long long u = 0; u < W; ++u) {
-        const long long gu = gr[u];
+    const size_t img = (size_t)b * H * W;
+    const int *gr = gT + img + row;                   // g(u) = gr[u * H]
+    int *S = stk + 2 * img + row, *T = S + (size_t)W * H;
+    auto at = [&](int *base, int q) -> int & { return base[(size_t)q * H]; };
+    int q = -1;
+    for (int u = 0; u < W; ++u) {
+        const int gu = gr[(size_t)u * H];
         if (gu >= inf) continue;
-        if (q < 0) {
-            q = 0;
-            s_at(0) = u;
-            t_at(0) = 0;
-            continue;
-        }
         while (q >= 0) {
-            const long long tq = t_at(q), sq = s_at(q);
-            const long long gs = gr[sq];
-            const long long f_old = (tq - sq) * (tq - sq) + gs * gs;
-            const long long f_new = (tq - u) * (tq - u) + gu * gu;
+            const int tq = at(T, q), sq = at(S, q);
+            const int gs = gr[(size_t)sq * H];
+            const int f_old = (tq - sq) * (tq - sq) + gs * gs;
+            const int f_new = (tq - u) * (tq - u) + gu * gu;
             if (f_old > f_new)
-                q -= 1;
+                --q;
             else
                 break;
         }
         if (q < 0) {
             q = 0;
-            s_at(0) = u;
-            t_at(0) = 0;
+            at(S, 0) = u;
+            at(T, 0) = 0;
         } else {
-            const long long sq = s_at(q);
-            const long long gs = gr[sq];
-            const long long wv = 1 + floordiv_pos(u * u - sq * sq + gu * gu - gs * gs, 2 * (u - sq));
+            const int sq = at(S, q), gs = gr[(size_t)sq * H];
+            const long long num = (long long)u * u - (long long)sq * sq + (long long)gu * gu - (long long)gs * gs;
+            const long long wv = 1 + floordiv_pos(num, 2LL * (u - sq));
             if (wv < W) {
-                q += 1;
-                s_at(q) = u;
-                t_at(q) = wv;
+                ++q;
+                at(S, q) = u;
+                at(T, q) = (int)wv;
             }
         }
     }
-    const size_t obase = ((size_t)b * H + row) * W;
-    const long long rb = min(row + 1, H - row);
-    for (long long u = W - 1; u >= 0; --u) {
-        long long d;
-        if (q < 0) {
-            d = inf;
-        } else {
-            const long long sq = s_at(q);
-            const long long dd = u - sq;
-            const long long gs = gr[sq];
+    int *o = outT + img + row;
+    for (int u = W - 1; u >= 0; --u) {
+        int d = inf;
+        if (q >= 0) {
+            const int sq = at(S, q), dd = u - sq, gs = gr[(size_t)sq * H];
             d = dd * dd + gs * gs;
-            if (u == t_at(q)) q -= 1;
+            if (u == at(T, q)) --q;
         }
-        if (out_mode == 1 || out_mode == 3) {   // morph.py:25-31 border term
-            const long long cb = min(u + 1, (long long)W - u);
-            const long long bb = min(rb, cb);
+        o[(size_t)u * H] = d;
+    }
+}
+
+// [n][W][H] int32 -> [n][H][W] output.  out_mode: 0 int64 distance;
+// 1 int64 min(distance, border^2) (morph.py:25-31); 2 uint8 distance <= thr
+// (dilate); 3 uint8 min(distance, border^2) > thr (erode)
+__global__ void transpose_out_kernel(const int *__restrict__ srcT, void *__restrict__ out, int H, int W, int out_mode,
+                                     long long thr) {
+    __shared__ int tile[32][33];
+    const size_t img = (size_t)blockIdx.z * H * W;
+    const int y0 = blockIdx.x * 32, x0 = blockIdx.y * 32;   // tile: rows y0.., columns x0..
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int x = x0 + j, y = y0 + threadIdx.x;
+        if (y < H && x < W) tile[j][threadIdx.x] = srcT[img + (size_t)x * H + y];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int y = y0 + j, x = x0 + threadIdx.x;
+        if (y >= H || x >= W) continue;
+        long long d = tile[threadIdx.x][j];
+        if (out_mode == 1 || out_mode == 3) {
+            const long long bb = min(min(y + 1, H - y), min(x + 1, W - x));
             d = min(d, bb * bb);
         }
+        const size_t o = img + (size_t)y * W + x;
         if (out_mode <= 1)
-            reinterpret_cast<long long *>(out)[obase + u] = d;
+            reinterpret_cast<long long *>(out)[o] = d;
         else if (out_mode == 2)
-            reinterpret_cast<uint8_t *>(out)[obase + u] = d <= thr ? 1 : 0;
+            reinterpret_cast<uint8_t *>(out)[o] = d <= thr ? 1 : 0;
         else
-            reinterpret_cast<uint8_t *>(out)[obase + u] = d > thr ? 1 : 0;
+            reinterpret_cast<uint8_t *>(out)[o] = d > thr ? 1 : 0;
     }
 }
 
@@ -174,17 +199,29 @@ __global__ void selftest_circuit_kernel(uint8_t *out84, uint8_t *out48) {
     }
 }
 
+// phase 1 alone (ts_edt_phase1_batch): int64 column distances, row-major
 cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
                               cudaStream_t st) {
     dim3 grid((W + 127) / 128, n);
-    edt_phase1_kernel<<<grid, 128, 0, st>>>(pix, g, n, H, W, invert, inf);
+    edt_phase1_kernel<long long><<<grid, 128, 0, st>>>(pix, g, n, H, W, invert, (int)inf);
     return cudaGetLastError();
 }
 
-cudaError_t launch_edt_phase2(const long long *g, void *out, long long *stk, int n, int H, int W, long long inf,
-                              int out_mode, long long thr, cudaStream_t st) {
-    dim3 grid((H + 63) / 64, n);
-    edt_phase2_kernel<<<grid, 64, 0, st>>>(g, out, stk, n, H, W, inf, out_mode, thr);
+// the exact EDT pipeline: phase 1 (or a caller's int64 g), transpose, phase 2
+// on rows, transpose back into the output.  scratch: 5 int32 per pixel.
+cudaError_t launch_edt(const uint8_t *pix, const long long *g64, void *out, int *scratch, int n, int H, int W,
+                       int invert, long long inf, int out_mode, long long thr, cudaStream_t st) {
+    const size_t px = (size_t)n * H * W;
+    int *g = scratch, *gT = scratch + px, *outT = g, *stk = scratch + 2 * px;   // outT reuses g
+    const dim3 tb(32, 8), tgrid((W + 31) / 32, (H + 31) / 32, n);
+    if (g64) {
+        transpose_in_kernel<long long><<<tgrid, tb, 0, st>>>(g64, gT, H, W);
+    } else {
+        edt_phase1_kernel<int><<<dim3((W + 127) / 128, n), 128, 0, st>>>(pix, g, n, H, W, invert, (int)inf);
+        transpose_in_kernel<int><<<tgrid, tb, 0, st>>>(g, gT, H, W);
+    }
+    edt_phase2T_kernel<<<dim3((H + 127) / 128, n), 128, 0, st>>>(gT, outT, stk, n, H, W, (int)inf);
+    transpose_out_kernel<<<dim3((H + 31) / 32, (W + 31) / 32, n), tb, 0, st>>>(outT, out, H, W, out_mode, thr);
     return cudaGetLastError();
 }
 
