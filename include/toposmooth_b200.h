@@ -36,7 +36,7 @@ extern "C" {
 #define TS_ERR_VALUE 1        /* invalid argument / input (reference ValueError) */
 #define TS_ERR_CUDA 2         /* CUDA runtime failure */
 #define TS_ERR_INTERNAL 3     /* device-side invariant violated (never silently truncates) */
-#define TS_ERR_UNSUPPORTED 4  /* outside the device path's limits (e.g. r > 16) */
+#define TS_ERR_UNSUPPORTED 4  /* outside the device path's limits (e.g. h, w > 32767 for r > 16) */
 
 /* Library version, e.g. 100 for 0.1.0. */
 int ts_version(void);
@@ -44,7 +44,10 @@ int ts_version(void);
 /* Message of the last failing call on this thread ("" if none). */
 const char *ts_last_error(void);
 
-/* Largest radius the fused HASF kernel is instantiated for (16). */
+/* Largest radius the fused single-launch HASF kernel is instantiated for
+ * (16).  Every radius is supported: above it, each stage runs as exact EDT ->
+ * stage mask -> the int64-priority engine (several launches per radius;
+ * images up to 32767 x 32767; ts_hasf_batch_async rejects r > 16). */
 int ts_max_radius(void);
 
 /* HASF: alternate homotopic cutting and filling at radii 1..r_max.

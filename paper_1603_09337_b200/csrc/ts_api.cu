@@ -29,11 +29,15 @@ cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, in
                               cudaStream_t st);
 cudaError_t launch_edt(const uint8_t *pix, const long long *g64, void *out, int *scratch, int n, int H, int W,
                        int invert, long long inf, int out_mode, long long thr, cudaStream_t st);
+cudaError_t launch_stage_mask(const long long *dist, const uint8_t *a, const uint8_t *b, uint8_t *out, size_t px,
+                              long long thr, int mode, cudaStream_t st);
 cudaError_t launch_classify(const uint8_t *pix, uint8_t *out, int n, int H, int W, const uint8_t *lut,
                             cudaStream_t st);
 cudaError_t launch_selftest_circuit(uint8_t *out84, uint8_t *out48, cudaStream_t st);
 cudaError_t launch_p4_to_rows(const uint8_t *p4, uint32_t *rows, long long nrows, int w, cudaStream_t st);
 cudaError_t launch_rows_to_p4(const uint32_t *rows, uint8_t *p4, long long nrows, int w, cudaStream_t st);
+cudaError_t launch_p4_to_u8(const uint8_t *p4, uint8_t *out, long long nrows, int w, cudaStream_t st);
+cudaError_t launch_u8_to_p4(const uint8_t *in, uint8_t *p4, long long nrows, int w, cudaStream_t st);
 cudaError_t launch_ccl(const uint8_t *img, int *parent, long long *counts, int n, int h, int w, int conn,
                        int target, int exterior, cudaStream_t st);
 }  // namespace ts
@@ -402,9 +406,9 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
                  const unsigned *ready = nullptr, unsigned *done = nullptr, int chunk = 1, int packed_io = 0) {
     int rc;
     if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
-    if (r_last > kMaxR)
-        return fail(TS_ERR_UNSUPPORTED, "radius " + std::to_string(r_last) + " exceeds the device path's maximum " +
-                                            std::to_string(kMaxR));
+    if (mode == MODE_HASF && r_last > kMaxR)
+        return fail(TS_ERR_UNSUPPORTED, "radius " + std::to_string(r_last) + " exceeds the fused kernel's maximum " +
+                                            std::to_string(kMaxR) + " (use the stage path)");
     if (n == 0) return ok();
     Plan pl;
     if ((rc = make_plan(h, w, r_last, mode, keep != nullptr, avoid != nullptr, fg, pl))) return rc;
@@ -548,6 +552,92 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     return ok();
 }
 
+// ---- radii above the fused kernel's kMaxR: one launch sequence per stage ----
+// The fused kernel instantiates its clamped bit-parallel EDT for r <= kMaxR.
+// Larger radii (the reference accepts any r >= 0, morph.py:18-22) run each
+// stage of smoothing.py:107-146 as: exact EDT (int64, border term for the
+// thinning priority) -> stage mask (F or V) -> the same engine in its int64-
+// priority mode (MODE_THIN / MODE_THICKEN, the homotopic_thin / _thicken
+// parity surfaces).  X is updated in place in `x` (device [n,h,w] uint8).
+int hasf_stages(uint8_t *x, int64_t n, int32_t h, int32_t w, int r_first, int r_last, int do_cut, int do_fill, int fg,
+                const uint8_t *keep, const uint8_t *avoid, cudaStream_t st) {
+    if (r_first > r_last) return ok();
+    if (h > 32767 || w > 32767) return fail(TS_ERR_UNSUPPORTED, "radius above the fused path needs h, w <= 32767");
+    const size_t px = (size_t)n * h * w;
+    const long long inf = (long long)h * h + (long long)w * w + 1;
+    char *ws = nullptr;
+    // dist int64 | EDT scratch 4 x int32 | mask | saved plane | engine output
+    TS_CUDA(ws_malloc((void **)&ws, px * (8 + 16 + 3), st));
+    long long *dist = reinterpret_cast<long long *>(ws);
+    int *scratch = reinterpret_cast<int *>(ws + 8 * px);
+    uint8_t *mask = reinterpret_cast<uint8_t *>(ws + 24 * px), *saved = mask + px, *y = saved + px;
+    int rc = TS_OK;
+    cudaError_t e = cudaSuccess;
+    auto edt = [&](const uint8_t *img, int background) {   // background: P = min(EDT(~img), B); else D = EDT(img)
+        if (e == cudaSuccess) e = launch_edt(img, nullptr, dist, scratch, (int)n, h, w, background, inf, background, 0, st);
+    };
+    auto mk = [&](const uint8_t *a, const uint8_t *b, long long thr, int mode) {
+        if (e == cudaSuccess) e = launch_stage_mask(dist, a, b, mask, px, thr, mode, st);
+    };
+    auto engine = [&](int emode, const uint8_t *img) {   // y = FLIP(img), then img <- y
+        if (e != cudaSuccess || rc) return;
+        rc = run_fused(emode, img, y, n, h, w, 1, 0, 0, 0, fg, mask, nullptr, reinterpret_cast<const int64_t *>(dist),
+                       -1, st, nullptr);
+        if (!rc) e = cudaMemcpyAsync(const_cast<uint8_t *>(img), y, px, cudaMemcpyDeviceToDevice, st);
+    };
+    for (int r = r_first; r <= r_last && e == cudaSuccess && rc == TS_OK; ++r) {
+        const long long r2 = (long long)r * r;
+        if (do_cut) {   // smoothing.py:127-135
+            if (e == cudaSuccess) e = cudaMemcpyAsync(saved, x, px, cudaMemcpyDeviceToDevice, st);
+            edt(x, 1);
+            mk(keep, nullptr, r2, 0);        // F = (P > r^2) | keep
+            engine(MODE_THIN, x);            // Y
+            edt(x, 0);
+            mk(saved, nullptr, r2, 1);       // V = (D <= r^2) & X
+            engine(MODE_THICKEN, x);
+        }
+        if (do_fill) {   // smoothing.py:138-146
+            if (e == cudaSuccess) e = cudaMemcpyAsync(saved, x, px, cudaMemcpyDeviceToDevice, st);
+            edt(x, 0);
+            mk(nullptr, avoid, r2, 2);       // V = (D <= r^2) & ~avoid
+            engine(MODE_THICKEN, x);         // Z
+            edt(x, 1);
+            mk(saved, nullptr, r2, 0);       // F = (P > r^2) | X
+            engine(MODE_THIN, x);
+        }
+    }
+    const std::string keep_msg = g_err;
+    cudaFreeAsync(ws, st);
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (rc) {
+        g_err = keep_msg;
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "stage path");
+    if (se != cudaSuccess) return cuda_fail(se, "stage path");
+    return ok();
+}
+
+// HASF over radii r_first..r_last: the fused kernel up to kMaxR, the stage
+// path beyond (validation happens in the first launch)
+int run_hasf_any(const uint8_t *in, uint8_t *out, int64_t n, int32_t h, int32_t w, int r_first, int r_last, int do_cut,
+                 int do_fill, int fg, const uint8_t *keep, const uint8_t *avoid, cudaStream_t st,
+                 int64_t *stats_host) {
+    if (r_last <= kMaxR)
+        return run_fused(MODE_HASF, in, out, n, h, w, r_first, r_last, do_cut, do_fill, fg, keep, avoid, nullptr, -1,
+                         st, stats_host);
+    int rc;
+    if ((rc = check_shape(n, h, w)) || (rc = check_fg(fg))) return rc;
+    if (n == 0) return ok();
+    // radii up to kMaxR fused (also validates input and constraints); with
+    // r_first > kMaxR a zero-radius pass only validates and copies
+    const int fl = std::min(r_last, kMaxR);
+    rc = run_fused(MODE_HASF, in, out, n, h, w, r_first <= kMaxR ? r_first : 1, r_first <= kMaxR ? fl : 0, do_cut,
+                   do_fill, fg, keep, avoid, nullptr, -1, st, stats_host);
+    if (rc) return rc;
+    return hasf_stages(out, n, h, w, std::max(r_first, kMaxR + 1), r_last, do_cut, do_fill, fg, keep, avoid, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -588,8 +678,8 @@ int ts_hasf_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h,
                   int32_t fg, const uint8_t *keep_dev, const uint8_t *avoid_dev, void *stream,
                   int64_t *stats_host) {
     if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
-    return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr, -1,
-                     (cudaStream_t)stream, stats_host);
+    return run_hasf_any(in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, (cudaStream_t)stream,
+                        stats_host);
 }
 
 // Non-blocking variant for callers whose buffers already live on the device:
@@ -601,6 +691,7 @@ int ts_hasf_batch_async(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int3
                         int32_t *err_dev) {
     if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
     if (!err_dev) return fail(TS_ERR_VALUE, "err_dev is required");
+    if (r_max > kMaxR) return fail(TS_ERR_UNSUPPORTED, "the non-blocking entry runs radii <= 16 (fused kernel)");
     cudaStream_t st = (cudaStream_t)stream;
     TS_CUDA(cudaMemsetAsync(err_dev, 0, sizeof(int32_t), st));
     return fused_launch(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr, -1, st,
@@ -973,6 +1064,28 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
     if (n == 0) return ok();
     cudaStream_t user = (cudaStream_t)stream;
     const size_t img = (size_t)h * w, bytes = (size_t)n * img;
+    if (r_max > kMaxR) {   // radii above the fused kernel: copy in, the stage path, copy out
+        const int nb = 2 + (keep_host ? 1 : 0) + (avoid_host ? 1 : 0);
+        uint8_t *d = nullptr;
+        TS_CUDA(ws_malloc((void **)&d, bytes * nb, user));
+        uint8_t *di = d, *dout = d + bytes, *dk = keep_host ? d + 2 * bytes : nullptr;
+        uint8_t *da = avoid_host ? d + (2 + (keep_host ? 1 : 0)) * bytes : nullptr;
+        cudaError_t e = cudaMemcpyAsync(di, in_host, bytes, cudaMemcpyHostToDevice, user);
+        if (e == cudaSuccess && dk) e = cudaMemcpyAsync(dk, keep_host, bytes, cudaMemcpyHostToDevice, user);
+        if (e == cudaSuccess && da) e = cudaMemcpyAsync(da, avoid_host, bytes, cudaMemcpyHostToDevice, user);
+        rc = e == cudaSuccess ? run_hasf_any(di, dout, n, h, w, 1, r_max, 1, 1, fg, dk, da, user, nullptr) : TS_OK;
+        if (e == cudaSuccess && rc == TS_OK) e = cudaMemcpyAsync(out_host, dout, bytes, cudaMemcpyDeviceToHost, user);
+        const std::string keep_msg = g_err;
+        cudaFreeAsync(d, user);
+        cudaError_t se = cudaStreamSynchronize(user);
+        if (rc) {
+            g_err = keep_msg;
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "host entry (stage path)");
+        if (se != cudaSuccess) return cuda_fail(se, "host entry (stage path)");
+        return ok();
+    }
     const bool big = (long long)h * w > 1024LL * 1024;   // team-sized images: one chunk
     const MemOps &mo = memops();
     // the streamed entry needs the copy engine to run while the kernel waits
@@ -1069,15 +1182,15 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
 int ts_cutting_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r, int32_t fg,
                      const uint8_t *keep_dev, void *stream) {
     if (r < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
-    return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, r == 0 ? 1 : r, r, 1, 0, fg, keep_dev, nullptr, nullptr,
-                     -1, (cudaStream_t)stream, nullptr);
+    return run_hasf_any(in_dev, out_dev, n, h, w, r == 0 ? 1 : r, r, 1, 0, fg, keep_dev, nullptr,
+                        (cudaStream_t)stream, nullptr);
 }
 
 int ts_filling_batch(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int32_t h, int32_t w, int32_t r, int32_t fg,
                      const uint8_t *avoid_dev, void *stream) {
     if (r < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");
-    return run_fused(MODE_HASF, in_dev, out_dev, n, h, w, r == 0 ? 1 : r, r, 0, 1, fg, nullptr, avoid_dev, nullptr,
-                     -1, (cudaStream_t)stream, nullptr);
+    return run_hasf_any(in_dev, out_dev, n, h, w, r == 0 ? 1 : r, r, 0, 1, fg, nullptr, avoid_dev,
+                        (cudaStream_t)stream, nullptr);
 }
 
 int ts_thin_batch(const uint8_t *img_dev, const uint8_t *keep_dev, const int64_t *prio_dev, uint8_t *out_dev,
@@ -1225,6 +1338,27 @@ int ts_hasf_batch_p4(const uint8_t *p4_in_dev, uint8_t *p4_out_dev, int64_t n, i
     if (r_max < 0) return fail(TS_ERR_VALUE, "ball radius must be >= 0");   // morph.py:18-22
     if (n == 0) return ok();
     cudaStream_t st = (cudaStream_t)stream;
+    if (r_max > kMaxR) {   // stage path (bytes): P4 -> uint8 planes -> HASF -> P4
+        const size_t px = (size_t)n * h * w;
+        uint8_t *b = nullptr;
+        TS_CUDA(ws_malloc((void **)&b, px * 4, st));
+        uint8_t *bi = b, *bo = b + px, *bk = keep_p4_dev ? b + 2 * px : nullptr, *ba = avoid_p4_dev ? b + 3 * px : nullptr;
+        cudaError_t e = launch_p4_to_u8(p4_in_dev, bi, n * h, w, st);
+        if (e == cudaSuccess && bk) e = launch_p4_to_u8(keep_p4_dev, bk, n * h, w, st);
+        if (e == cudaSuccess && ba) e = launch_p4_to_u8(avoid_p4_dev, ba, n * h, w, st);
+        rc = e == cudaSuccess ? run_hasf_any(bi, bo, n, h, w, 1, r_max, 1, 1, fg, bk, ba, st, nullptr) : TS_OK;
+        if (e == cudaSuccess && rc == TS_OK) e = launch_u8_to_p4(bo, p4_out_dev, n * h, w, st);
+        const std::string keep_msg = g_err;
+        cudaFreeAsync(b, st);
+        cudaError_t se = cudaStreamSynchronize(st);
+        if (rc) {
+            g_err = keep_msg;
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "P4 path");
+        if (se != cudaSuccess) return cuda_fail(se, "P4 path");
+        return ok();
+    }
     const int ww = (w + 31) / 32;
     const size_t words = (size_t)n * h * ww;
     char *ws = nullptr;

@@ -154,6 +154,35 @@ __global__ void transpose_out_kernel(const int *__restrict__ srcT, void *__restr
     }
 }
 
+// Stage masks of the multi-launch HASF path (radii above the fused kernel's
+// kMaxR, smoothing.py:107-146): mode 0 F = (dist > thr) | a (thinning floor,
+// a = keep or the filling's input, may be null); mode 1 V = (dist <= thr) & a
+// (cutting's regrowth cap, a = X); mode 2 V = (dist <= thr) & ~b (filling's
+// cap, b = avoid, may be null).
+__global__ void stage_mask_kernel(const long long *__restrict__ dist, const uint8_t *__restrict__ a,
+                                  const uint8_t *__restrict__ b, uint8_t *__restrict__ out, size_t px, long long thr,
+                                  int mode) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < px; i += (size_t)gridDim.x * blockDim.x) {
+        const long long d = dist[i];
+        uint8_t v;
+        if (mode == 0)
+            v = (d > thr) | (a ? a[i] : 0);
+        else if (mode == 1)
+            v = (d <= thr) & a[i];
+        else
+            v = (d <= thr) & (b ? (uint8_t)(b[i] ^ 1) : (uint8_t)1);
+        out[i] = v;
+    }
+}
+
+cudaError_t launch_stage_mask(const long long *dist, const uint8_t *a, const uint8_t *b, uint8_t *out, size_t px,
+                              long long thr, int mode, cudaStream_t st) {
+    size_t nb = (px + 255) / 256;
+    const int blocks = (int)(nb < 148 * 16 ? (nb < 1 ? 1 : nb) : 148 * 16);
+    stage_mask_kernel<<<blocks, 256, 0, st>>>(dist, a, b, out, px, thr, mode);
+    return cudaGetLastError();
+}
+
 // 8-bit neighbour code per pixel (topo.py:97-106); optional simple mask via a
 // 256-entry LUT staged in shared memory (topo.py:144-148)
 __global__ void classify_kernel(const uint8_t *__restrict__ pix, uint8_t *__restrict__ out, int n, int H, int W,

@@ -50,6 +50,32 @@ __global__ void rows_to_p4_kernel(const uint32_t *__restrict__ rows, uint8_t *__
     }
 }
 
+// P4 raster <-> uint8 {0,1} planes (the stage path for radii above kMaxR works on bytes)
+__global__ void p4_to_u8_kernel(const uint8_t *__restrict__ p4, uint8_t *__restrict__ out, long long nrows, int w,
+                                int row_bytes) {
+    const long long total = nrows * w;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / w;
+        const int c = (int)(i - r * w);
+        out[i] = (p4[r * row_bytes + (c >> 3)] >> (7 - (c & 7))) & 1u;
+    }
+}
+
+__global__ void u8_to_p4_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ p4, long long nrows, int w,
+                                int row_bytes) {
+    const long long total = nrows * row_bytes;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / row_bytes;
+        const int c0 = (int)(i - r * row_bytes) * 8;
+        uint32_t v = 0;
+        for (int k = 0; k < 8; ++k)
+            if (c0 + k < w) v |= (uint32_t)(in[r * w + c0 + k] & 1u) << (7 - k);
+        p4[i] = (uint8_t)v;
+    }
+}
+
 static int grid_for(long long work) {
     long long g = (work + 255) / 256;
     return (int)(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
@@ -64,6 +90,16 @@ cudaError_t launch_p4_to_rows(const uint8_t *p4, uint32_t *rows, long long nrows
 cudaError_t launch_rows_to_p4(const uint32_t *rows, uint8_t *p4, long long nrows, int w, cudaStream_t st) {
     const int ww = (w + 31) / 32, rb = (w + 7) / 8;
     rows_to_p4_kernel<<<grid_for(nrows * ww), 256, 0, st>>>(rows, p4, nrows, w, rb, ww);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p4_to_u8(const uint8_t *p4, uint8_t *out, long long nrows, int w, cudaStream_t st) {
+    p4_to_u8_kernel<<<grid_for(nrows * w), 256, 0, st>>>(p4, out, nrows, w, (w + 7) / 8);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_u8_to_p4(const uint8_t *in, uint8_t *p4, long long nrows, int w, cudaStream_t st) {
+    u8_to_p4_kernel<<<grid_for(nrows * ((w + 7) / 8)), 256, 0, st>>>(in, p4, nrows, w, (w + 7) / 8);
     return cudaGetLastError();
 }
 

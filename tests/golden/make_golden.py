@@ -253,8 +253,42 @@ def gen_netpbm():
     np.savez_compressed(os.path.join(HERE, "netpbm.npz"), **d)
 
 
+def gen_hasf_big_r():
+    """Radii above the fused kernel's 16 (reference accepts any r >= 0,
+    morph.py:18-22): hasf up to r_max 17..22 and single cutting / filling
+    halves at r = 17..25, both adjacencies, with constraints."""
+    rng = np.random.default_rng(7010)
+    d, names = {}, []
+    for i in range(6):
+        h, w = int(rng.integers(40, 90)), int(rng.integers(40, 90))
+        img = (rng.random((h, w)) < 0.55).astype(np.uint8)
+        fg = 8 if i % 2 == 0 else 4
+        r = 17 + i
+        keep = (img & (rng.random((h, w)) < 0.02)).astype(np.uint8) if i % 3 == 0 else None
+        avoid = (((rng.random((h, w)) < 0.02) & (img == 0)).astype(np.uint8)) if i % 3 == 1 else None
+        out = ts.hasf(img, ts.SmoothingConfig(r_max=r, adj=adj_of(fg), keep=keep, avoid=avoid))
+        k = f"h{i}"
+        names.append(k)
+        d[f"{k}_shape"] = np.array(img.shape)
+        d[f"{k}_img"], _ = pack(img)
+        d[f"{k}_out"], _ = pack(out)
+        d[f"{k}_r"] = np.array(r)
+        d[f"{k}_fg"] = np.array(fg)
+        if keep is not None:
+            d[f"{k}_keep"], _ = pack(keep)
+        if avoid is not None:
+            d[f"{k}_avoid"], _ = pack(avoid)
+        cut = ts.homotopic_cutting(img, np.zeros_like(img), 20 + i, adj_of(fg))
+        fil = ts.homotopic_filling(img, np.zeros_like(img), 20 + i, adj_of(fg))
+        d[f"{k}_cut"], _ = pack(cut)
+        d[f"{k}_fill"], _ = pack(fil)
+    d["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "hasf_big_r.npz"), **d)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["lut", "sep", "edt", "morph", "engine", "halves", "hasf_small", "hasf_configs", "netpbm"]
+    which = sys.argv[1:] or ["lut", "sep", "edt", "morph", "engine", "halves", "hasf_small", "hasf_configs", "netpbm",
+                             "hasf_big_r"]
     for name in which:
         t0 = time.perf_counter()
         globals()[f"gen_{name}"]()

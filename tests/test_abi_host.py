@@ -42,7 +42,7 @@ def test_library_is_sm100a_cubin():
 def test_version_and_limits():
     lib = _lib.load()
     assert lib.ts_version() == 100
-    assert lib.ts_max_radius() == 16
+    assert lib.ts_max_radius() == 16   # the fused single-launch path; larger radii run per stage
 
 
 def test_connectivity_tables_match_reference():

@@ -173,8 +173,33 @@ def test_device_validation_errors():
     avoid[1, 2, 2] = 1
     with pytest.raises(ValueError, match="avoid-constraint"):
         P.hasf_batch(imgs, 1, avoid=avoid)
-    with pytest.raises(RuntimeError, match="exceeds"):
-        P.smooth(np.zeros((8, 8), np.uint8), 17)
+    # radii above the fused kernel (16) run the stage path: same validation
+    with pytest.raises(ValueError, match="keep-constraint"):
+        P.hasf_batch(np.zeros((2, 8, 8), np.uint8), 17, keep=keep)
+    assert np.array_equal(P.smooth(np.zeros((8, 8), np.uint8), 17), np.zeros((8, 8), np.uint8))
+
+
+def test_big_radii_golden():
+    """Radii 17..25 (reference accepts any r >= 0, morph.py:18-22): the fused
+    kernel up to 16, then per-stage launches (exact EDT -> stage mask -> the
+    int64-priority engine), against reference goldens; also through the host,
+    P4 and batched entries."""
+    for c in golden_cases("hasf_big_r"):
+        adj = P.ADJ_84 if c["fg"] == 8 else P.ADJ_48
+        cfg = P.SmoothingConfig(r_max=c["r"], adj=adj, keep=c.get("keep"), avoid=c.get("avoid"))
+        assert np.array_equal(P.hasf(c["img"], cfg), c["out"]), c["name"]
+        r2 = 20 + int(c["name"][1:])
+        z = np.zeros_like(c["img"])
+        assert np.array_equal(P.homotopic_cutting(c["img"], z, r2, adj), c["cut"]), c["name"]
+        assert np.array_equal(P.homotopic_filling(c["img"], z, r2, adj), c["fill"]), c["name"]
+        if c.get("keep") is None and c.get("avoid") is None:
+            imgs = np.stack([c["img"]] * 3)
+            assert np.array_equal(P.hasf_batch_host(imgs, c["r"], adj)[2], c["out"]), c["name"]
+            w = c["img"].shape[1]
+            got = P.hasf_p4(np.packbits(imgs, axis=2), w, c["r"], adj)
+            assert np.array_equal(np.unpackbits(got, axis=2)[1, :, :w], c["out"]), c["name"]
+    img = W.config_image("c1", 7)[:200, :200].copy()
+    assert np.array_equal(P.smooth(img, 18), O.hasf(img, 18, 8))
 
 
 def test_topology_invariants_full_size_batches():

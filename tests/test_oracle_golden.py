@@ -103,3 +103,11 @@ def test_large_goldens_inputs_and_oracle_c2():
         assert sha(W.config_image(cfg, i)) == str(z[f"c2_{i}_in_sha"])
     img = W.config_image(cfg, 31)
     assert sha(O.hasf(img, cfg.r_max, 8)) == str(z["c2_31_out_sha"])
+
+
+def test_oracle_big_radii_golden():
+    """Radii above 16 (reference hasf / homotopic_cutting / homotopic_filling)."""
+    for c in golden_cases("hasf_big_r"):
+        keep = c.get("keep")
+        avoid = c.get("avoid")
+        assert np.array_equal(O.hasf(c["img"], c["r"], c["fg"], keep=keep, avoid=avoid), c["out"]), c["name"]
