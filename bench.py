@@ -362,6 +362,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: = steps")
     ap.add_argument("--verify", type=int, default=2, help="images checked bit-exact vs the oracle")
+    ap.add_argument("--cluster-teams", type=int, default=1,
+                    help="teams of 2..8 CTAs (large images) as thread-block clusters (1) or cooperative launches (0)")
     ap.add_argument("--host-streaming", type=int, default=1,
                     help="e2e host entry: 1 = one launch fed by streamed chunks, 0 = chunked launches")
     args = ap.parse_args()
@@ -386,6 +388,7 @@ def main():
         dist.init_process_group("nccl", init_method="env://")
     if args.smem_budget >= 0:
         _lib.load().ts_set_smem_budget(args.smem_budget)
+    _lib.load().ts_set_cluster_teams(args.cluster_teams)
     adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
 
     # this rank's images: indices rank*n .. rank*n + n - 1 (distinct seeds, weak scaling)

@@ -172,6 +172,14 @@ int ts_hasf_batch_p4(const uint8_t *p4_in_dev, uint8_t *p4_out_dev, int64_t n, i
  * fewer images than co-resident CTAs).  Returns the previous value. */
 int32_t ts_set_team_size(int32_t ctas);
 
+/* Tuning / A-B: 1 (default) = teams of 2..8 CTAs (large images, e.g. c2's
+ * 2048^2 with 4 CTAs each) run as thread-block clusters: hardware cluster
+ * barriers instead of the global-atomic team barrier, and the team's control
+ * block (queues' counters, list lengths) in the rank-0 CTA's shared memory,
+ * reached by the others over distributed shared memory; 0 = cooperative
+ * launch with the global control block.  Returns the previous value. */
+int32_t ts_set_cluster_teams(int32_t on);
+
 /* Tuning/testing: force the kernel flavour, 512 threads x 1 CTA/SM or 256 x 2
  * (0 = automatic: 256 x 2 when the hot planes fit half an SM).  Returns the previous value. */
 int32_t ts_set_cta_threads(int32_t threads);

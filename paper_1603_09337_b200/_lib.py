@@ -51,6 +51,7 @@ SIGNATURES = {
     "ts_set_smem_budget": ([_i64], _i64),
     "ts_set_dense_divisor": ([_i32], _i32),
     "ts_set_team_size": ([_i32], _i32),
+    "ts_set_cluster_teams": ([_i32], _i32),
     "ts_set_cta_threads": ([_i32], _i32),
     "ts_set_host_streaming": ([_i32], _i32),
     "ts_set_fused_prep": ([_i32], _i32),

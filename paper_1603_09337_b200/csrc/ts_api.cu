@@ -25,6 +25,7 @@
 namespace ts {
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream);
 cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm);
+cudaError_t hasf_cluster_occupancy(int fg, size_t smem_bytes, int team, int *clusters);
 cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
                               cudaStream_t st);
 cudaError_t launch_edt(const uint8_t *pix, const long long *g64, void *out, int *scratch, int n, int H, int W,
@@ -239,6 +240,7 @@ int device_props(int *sms, int *smem_optin, int *smem_per_sm) {
 }
 
 std::atomic<int> g_team_knob{0};   // 0 = automatic team size
+std::atomic<int> g_cluster_knob{1};   // teams of 2..8 CTAs as thread-block clusters
 
 // team = CTAs per image (> 1 only with every plane in global memory)
 std::atomic<int> g_threads_knob{0};   // 0 = automatic kernel flavour
@@ -427,7 +429,21 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
         if (team > pt.per_wave) return fail(TS_ERR_UNSUPPORTED, "team larger than the co-resident CTA count");
         pl = pt;
     }
-    const int teams = (int)std::min<long long>(n, pl.per_wave / team);
+    // teams of 2..8 CTAs run as thread-block clusters (hardware barriers, the
+    // control block in DSMEM); larger teams (c3: one image over every SM) use
+    // the cooperative launch with a global barrier
+    bool cluster = false;
+    int max_teams = pl.per_wave / team;
+    if (team >= 2 && team <= 8 && g_cluster_knob.load()) {
+        int nc = 0;
+        if (hasf_cluster_occupancy(fg, pl.smem_bytes, team, &nc) == cudaSuccess && nc >= 1) {
+            cluster = true;
+            max_teams = std::min(max_teams, nc);
+        } else {
+            cudaGetLastError();
+        }
+    }
+    const int teams = (int)std::min<long long>(n, max_teams);
     const int grid = teams * team;
     // segmented scheduling: a batch larger than one wave of single-CTA images
     // is handed out as (segment, image) tasks, so the last wave's idle SMs are
@@ -446,7 +462,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
         nseg = seg_count(total_stages, seg_stages, fine);
     const size_t ws_words = (size_t)pl.stride_ws * (team > 1 ? teams : grid);
     const size_t xbuf_words = nseg > 1 ? (size_t)n * 4 * h * pl.WW : 0;   // image, XS, keep, avoid
-    const size_t tctl_bytes = team > 1 ? (size_t)teams * kTeamCtlBytes : 0;
+    const size_t tctl_bytes = team > 1 && !cluster ? (size_t)teams * kTeamCtlBytes : 0;
     const size_t stats_bytes = stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0;
     const size_t prog_bytes = nseg > 1 ? (((size_t)n * sizeof(unsigned) + 63) & ~(size_t)63) : 0;
     const size_t ctrl_bytes = 64 + stats_bytes + prog_bytes + tctl_bytes;
@@ -498,7 +514,8 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.stats = stats_host ? reinterpret_cast<long long *>(ctrl + 64) : nullptr;
     p.team = team;
     p.threads = pl.threads;
-    p.tctl = team > 1 ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
+    p.tctl = tctl_bytes ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
+    p.cluster = cluster ? 1 : 0;
     p.fused = pl.fused ? 1 : 0;
     p.packed_io = packed_io;
     p.ready = ready;
@@ -1038,6 +1055,8 @@ int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
 int32_t ts_set_segment_stages(int32_t stages) { return g_seg_stages.exchange(stages < 0 ? 0 : stages); }
 
 int32_t ts_set_segment_fine(int32_t stages) { return g_seg_fine.exchange(stages < 0 ? 0 : stages); }
+
+int32_t ts_set_cluster_teams(int32_t on) { return g_cluster_knob.exchange(on ? 1 : 0); }
 
 int32_t ts_set_host_segments(int32_t stages, int32_t fine) {
     g_seg_fine_host.store(fine < 0 ? 0 : fine);

@@ -9,7 +9,8 @@ namespace ts {
 
 #define TS_DECLARE_HASF_VARIANT(SUFFIX)                                                                   \
     cudaError_t launch_hasf_##SUFFIX(const KParams &p, int grid, size_t smem_bytes, cudaStream_t stream); \
-    cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks);
+    cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks);                                  \
+    cudaError_t clusters_hasf_##SUFFIX(size_t smem_bytes, int team, int *clusters);
 TS_DECLARE_HASF_VARIANT(8h)
 TS_DECLARE_HASF_VARIANT(8g)
 TS_DECLARE_HASF_VARIANT(4h)
@@ -40,6 +41,11 @@ cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, c
     }
     if (fg == 8) return p.hot ? launch_hasf_8h(p, grid, smem_bytes, stream) : launch_hasf_8g(p, grid, smem_bytes, stream);
     return p.hot ? launch_hasf_4h(p, grid, smem_bytes, stream) : launch_hasf_4g(p, grid, smem_bytes, stream);
+}
+
+// co-resident clusters of `team` CTAs of the global-placement variant
+cudaError_t hasf_cluster_occupancy(int fg, size_t smem_bytes, int team, int *clusters) {
+    return fg == 8 ? clusters_hasf_8g(smem_bytes, team, clusters) : clusters_hasf_4g(smem_bytes, team, clusters);
 }
 
 cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm) {

@@ -98,6 +98,14 @@ __device__ __forceinline__ int pidx(const Img &g, int y, int x) { return g.org +
 
 __device__ __forceinline__ void set_err(int *err, int code) { atomicCAS(err, 0, code); }
 
+// generic address of the same shared-memory variable in CTA `rank` of this
+// thread-block cluster (mapa: distributed shared memory)
+__device__ __forceinline__ void *dsmem_map(void *p, unsigned rank) {
+    void *r;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(p), "r"(rank));
+    return r;
+}
+
 // Barrier over the G CTAs of a team (co-resident: cooperative launch).  Thread 0
 // of each CTA arrives on a global counter; the last one resets it and bumps the
 // generation.  The gpu-scope fences order the CTA's writes before the arrival
@@ -107,6 +115,13 @@ __device__ __forceinline__ void set_err(int *err, int code) { atomicCAS(err, 0, 
 __device__ __forceinline__ void team_sync(const Img &g) {
     if (g.G == 1) {
         __syncthreads();
+        return;
+    }
+    if (g.bar == nullptr) {
+        // the team is a thread-block cluster: the hardware cluster barrier,
+        // release / acquire at cluster scope (planes written by one CTA of the
+        // team are read by the others after it)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         return;
     }
     __syncthreads();
@@ -1993,8 +2008,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     const int team = (int)blockIdx.x / G, rank = (int)blockIdx.x - team * G;
     uint32_t *cta = p.gws + (size_t)(G == 1 ? blockIdx.x : team) * (size_t)p.gws_stride;
     auto buf = [&](int b) -> uint32_t * { return ((p.smem_mask >> b) & 1u) ? smem + p.off[b] : cta + p.off[b]; };
-    TeamCtl *tc = G == 1 ? nullptr : reinterpret_cast<TeamCtl *>(p.tctl) + team;
-    Shared *shp = G == 1 ? &sh_local : &tc->sh;
+    // teams: a global control block (cooperative launch), or -- when the team
+    // is a thread-block cluster -- the control block of the team's rank-0 CTA,
+    // shared with the others over distributed shared memory (DSMEM)
+    TeamCtl *tc = (G == 1 || p.cluster) ? nullptr : reinterpret_cast<TeamCtl *>(p.tctl) + team;
+    Shared *shp = G == 1 ? &sh_local
+                         : (p.cluster ? reinterpret_cast<Shared *>(dsmem_map(&sh_local, 0)) : &tc->sh);
     View vl;   // built by every thread, published in shared memory: the noinline
                // phases take it by reference (no per-call copy to local memory)
     if constexpr (HOT) {
@@ -2042,6 +2061,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     __shared__ View v_shared;
     if (threadIdx.x == 0) v_shared = vl;
     __syncthreads();
+    if (!HOT && p.cluster) {   // rank 0's control block: zeroed, and every CTA of the cluster running
+        if (rank == 0 && threadIdx.x == 0) sh_local = Shared{};
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
     const View &v = v_shared;
     const Img gk = make_img<HOT>(v);   // team / sync view for this function
     Shared &sh = *shp;
@@ -2203,6 +2226,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             atomicAdd(p.done + img / p.chunk, 1u);
         }
     }
+    // cluster teams: no CTA leaves while another may still read rank 0's control block
+    if (!HOT && p.cluster)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // per-variant host entry points, one translation unit each (ts_hasf_<fg><h|g>.cu)
@@ -2223,9 +2249,42 @@ cudaError_t raise_smem_limit_once(const void *fn, std::mutex &mu, bool (&done)[6
         cudaError_t e = raise_smem_limit_once(fn, g_attr_mu_##SUFFIX, g_attr_done_##SUFFIX);                   \
         if (e != cudaSuccess) return e;                                                                         \
         void *args[] = {(void *)&p};                                                                            \
+        if (p.team > 1 && p.cluster) {                                                                          \
+            cudaLaunchConfig_t cfg{};                                                                           \
+            cudaLaunchAttribute at[1];                                                                          \
+            at[0].id = cudaLaunchAttributeClusterDimension;                                                     \
+            at[0].val.clusterDim.x = (unsigned)p.team;                                                          \
+            at[0].val.clusterDim.y = 1;                                                                         \
+            at[0].val.clusterDim.z = 1;                                                                         \
+            cfg.gridDim = dim3(grid);                                                                           \
+            cfg.blockDim = dim3(kThreads);                                                                      \
+            cfg.dynamicSmemBytes = smem_bytes;                                                                  \
+            cfg.stream = stream;                                                                                \
+            cfg.attrs = at;                                                                                     \
+            cfg.numAttrs = 1;                                                                                   \
+            return cudaLaunchKernelExC(&cfg, fn, args);                                                         \
+        }                                                                                                       \
         if (p.team > 1)                                                                                         \
             return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);      \
         return cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, smem_bytes, stream);                     \
+    }                                                                                                           \
+    cudaError_t clusters_hasf_##SUFFIX(size_t smem_bytes, int team, int *clusters) {                            \
+        using namespace TS_IMPL_NS;                                                                             \
+        const void *fn = (const void *)hasf_kernel<FG, HOT>;                                                    \
+        cudaError_t e = raise_smem_limit_once(fn, g_attr_mu_##SUFFIX, g_attr_done_##SUFFIX);                   \
+        if (e != cudaSuccess) return e;                                                                         \
+        cudaLaunchConfig_t cfg{};                                                                               \
+        cudaLaunchAttribute at[1];                                                                              \
+        at[0].id = cudaLaunchAttributeClusterDimension;                                                         \
+        at[0].val.clusterDim.x = (unsigned)team;                                                                \
+        at[0].val.clusterDim.y = 1;                                                                             \
+        at[0].val.clusterDim.z = 1;                                                                             \
+        cfg.gridDim = dim3(team * 64);                                                                          \
+        cfg.blockDim = dim3(kThreads);                                                                          \
+        cfg.dynamicSmemBytes = smem_bytes;                                                                      \
+        cfg.attrs = at;                                                                                         \
+        cfg.numAttrs = 1;                                                                                       \
+        return cudaOccupancyMaxActiveClusters(clusters, fn, &cfg);                                              \
     }                                                                                                           \
     cudaError_t occupancy_hasf_##SUFFIX(size_t smem_bytes, int *blocks) {                                       \
         using namespace TS_IMPL_NS;                                                                             \

@@ -98,7 +98,8 @@ struct KParams {
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
     int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
     int threads;            // threads per CTA of the variant (512, or 256 = two CTAs per SM)
-    void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1)
+    void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1, not a cluster)
+    int cluster;            // 1: each team is a thread-block cluster (control block in rank 0's smem, cluster barriers)
     int r_first, r_last, do_cut, do_fill;
     int mode;
     long long max_sweeps;   // < 0: unbounded

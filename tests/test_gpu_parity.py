@@ -236,11 +236,21 @@ def team_knob():
     lib.ts_set_team_size(0)
 
 
-@pytest.mark.parametrize("team", [2, 3, 5])
-def test_team_mode_vs_oracle(team_knob, team):
+@pytest.mark.parametrize("team,cluster", [(2, 1), (3, 1), (5, 1), (8, 1), (2, 0), (3, 0), (5, 0)])
+def test_team_mode_vs_oracle(team_knob, team, cluster):
     """Teams of CTAs sharing one image through L2 (the large-image path),
-    forced on small images so the oracle can check them."""
+    forced on small images so the oracle can check them: as thread-block
+    clusters (hardware barrier, control block over DSMEM) and as a
+    cooperative launch with the global barrier."""
     team_knob.ts_set_team_size(team)
+    old_cluster = team_knob.ts_set_cluster_teams(cluster)
+    try:
+        _team_cases(team)
+    finally:
+        team_knob.ts_set_cluster_teams(old_cluster)
+
+
+def _team_cases(team):
     rng = np.random.default_rng(100 + team)
     for (h, w, fg, r) in [(160, 200, 8, 3), (97, 130, 4, 2), (64, 64, 8, 4)]:
         imgs = np.stack([random_image(rng, h, w, rng.uniform(0.3, 0.7)) for _ in range(3)])

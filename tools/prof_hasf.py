@@ -42,7 +42,12 @@ def main():
     if args.threads > 0:
         _lib.load().ts_set_cta_threads(args.threads)
     args.n = args.n or cfg.n
-    imgs = torch.from_numpy(W.config_batch(cfg, args.start, args.n)).cuda()
+    imgs_np = W.config_batch(cfg, args.start, args.n)
+    imgs = torch.from_numpy(imgs_np).cuda()
+    keep = avoid = None
+    if cfg.constraints > 0:
+        k_, a_ = W.constraint_masks(cfg, imgs_np, args.start)
+        keep, avoid = torch.from_numpy(k_).cuda(), torch.from_numpy(a_).cuda()
     adj = P.ADJ_84 if cfg.fg == 8 else P.ADJ_48
     plan = np.zeros(6, np.int64)
     _lib.load().ts_hasf_plan(cfg.h, cfg.w, cfg.r_max, 0, 0, plan.ctypes.data)
@@ -51,9 +56,9 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if args.stats:
-            out, st = P.hasf_batch(imgs, cfg.r_max, adj, stats=True)
+            out, st = P.hasf_batch(imgs, cfg.r_max, adj, keep=keep, avoid=avoid, stats=True)
         else:
-            out = P.hasf_batch(imgs, cfg.r_max, adj)
+            out = P.hasf_batch(imgs, cfg.r_max, adj, keep=keep, avoid=avoid)
         e1.record()
         torch.cuda.synchronize()
         res[f"ms_{i}"] = e0.elapsed_time(e1)

@@ -96,8 +96,10 @@ def main():
     ap.add_argument("--bytes-per-image", type=int, default=0)
     ap.add_argument("--config", default="c1")
     ap.add_argument("--cmd", default="")
+    ap.add_argument("--out-dir", default=os.path.join(REPO, "profiles"),
+                    help="where the summaries go (on the GPU box: a gpurun_out/ subdirectory)")
     a = ap.parse_args()
-    prof = os.path.join(REPO, "profiles")
+    prof = a.out_dir
     os.makedirs(prof, exist_ok=True)
     if a.launches:
         with open(os.path.join(prof, f"{a.tag}_launches.txt"), "w") as fh:
