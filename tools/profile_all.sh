@@ -16,7 +16,7 @@ for c in ${CFGS:-c1 c4 c2 c0 c1k c3}; do
         --log-file $T/launches_$c.csv $B > $T/ncu_launch_$c.log 2>&1
     python tools/summarize_ncu.py --launches $T/launches_$c.csv --tag ${TAG}_$c --config $c --out-dir $O --cmd "$B"
   fi
-  P="python tools/prof_hasf.py --config $c --repeat 2 --stats 0"
+  P="python tools/prof_hasf.py --config $c --n 0 --repeat 2 --stats 0"
   $P > $T/prof_plain_$c.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:hasf_kernel \
       -s 1 -c 1 -o $T/full_$c -f $P > $T/ncu_full_$c.log 2>&1
   echo "$c: rc=$? $(tail -c 150 $T/ncu_full_$c.log | tr '\n' ' ')"
