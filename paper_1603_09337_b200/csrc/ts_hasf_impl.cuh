@@ -665,6 +665,10 @@ __device__ __forceinline__ uint32_t decide(uint32_t c, const Nb &i, const Nb &d,
 #define TS_DENSE_BATCH 2
 #endif
 constexpr int kDenseBatch = TS_DENSE_BATCH;
+#ifndef TS_DENSE_BATCH_L2
+#define TS_DENSE_BATCH_L2 2
+#endif
+constexpr int kDenseBatchL2 = TS_DENSE_BATCH_L2;   // rows whose C / E loads are in flight together (L2 planes)
 
 
 template <int FG>
@@ -800,13 +804,13 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, int pc, int &evals) 
                 e1 = ep[1];
             }
         };
-        while (y + kDenseBatch <= y1) {
-            uint32_t cb[kDenseBatch];
-            uint4 e0b[kDenseBatch], e1b[kDenseBatch];
+        while (y + kDenseBatchL2 <= y1) {
+            uint32_t cb[kDenseBatchL2];
+            uint4 e0b[kDenseBatchL2], e1b[kDenseBatchL2];
 #pragma unroll
-            for (int j = 0; j < kDenseBatch; ++j) fetch(p + j * g.S, cb[j], e0b[j], e1b[j]);
+            for (int j = 0; j < kDenseBatchL2; ++j) fetch(p + j * g.S, cb[j], e0b[j], e1b[j]);
 #pragma unroll
-            for (int j = 0; j < kDenseBatch; ++j) step(cb[j], e0b[j], e1b[j]);
+            for (int j = 0; j < kDenseBatchL2; ++j) step(cb[j], e0b[j], e1b[j]);
         }
         while (y < y1) {
             uint32_t c;
@@ -1863,7 +1867,10 @@ __device__ __forceinline__ void run_stage(const View &v, const Img &gt, int r, b
 }
 
 // bit rows [H][WW] (host- or P4-packed, or a segment's saved state) into a
-// plane; the strip's words are requested together (one latency per batch)
+// plane; the strip's words are requested together (one latency per batch).
+// Plain (L1-cached) loads: a segment's state written on another SM is read
+// only after the lead's ld.acquire.gpu (which invalidates this SM's L1,
+// CCTL.IVALL) and a CTA barrier.
 __device__ __forceinline__ void load_rows(const Img &g, const uint32_t *from, uint32_t *to) {
     walk_strips(g, [&](int x, int y0, int y1, int) {
         constexpr int kB = 16;
@@ -1871,7 +1878,7 @@ __device__ __forceinline__ void load_rows(const Img &g, const uint32_t *from, ui
             uint32_t w[kB];
 #pragma unroll
             for (int j = 0; j < kB; ++j)
-                if (yb + j < y1) w[j] = __ldcg(from + (size_t)(yb + j) * g.WW + x);
+                if (yb + j < y1) w[j] = from[(size_t)(yb + j) * g.WW + x];
 #pragma unroll
             for (int j = 0; j < kB; ++j)
                 if (yb + j < y1) to[pidx(g, yb + j, x)] = w[j];
@@ -1975,13 +1982,27 @@ __device__ __noinline__ void store_state_nl(const View &v, uint32_t *dst, bool w
     const Img g = make_img<HOT>(v);
     const size_t wimg = (size_t)g.H * g.WW;
     // slots: 0 the image, 1 XS, 2 / 3 keep / avoid packed once (first segment)
-    for_strip(g, [&](int y, int x, int q) {
-        const size_t o = (size_t)y * g.WW + x;
-        __stcg(dst + o, g.I[q]);
-        if (with_xs) __stcg(dst + wimg + o, g.XS[q]);
-        if (with_k) __stcg(dst + 2 * wimg + o, g.K[q]);
-        if (with_a) __stcg(dst + 3 * wimg + o, g.A[q]);
-    });
+    // plain stores (L1 is write-through): ordered before the lead's release
+    // by the CTA barrier and its __threadfence; planes that may live in L2
+    // are read in batches (one latency per batch)
+    auto out = [&](const uint32_t *plane, uint32_t *to) {
+        walk_strips(g, [&](int x, int y0, int y1, int) {
+            constexpr int kB = 16;
+            for (int yb = y0; yb < y1; yb += kB) {
+                uint32_t w[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+                    if (yb + j < y1) w[j] = plane[pidx(g, yb + j, x)];
+#pragma unroll
+                for (int j = 0; j < kB; ++j)
+                    if (yb + j < y1) to[(size_t)(yb + j) * g.WW + x] = w[j];
+            }
+        });
+    };
+    out(g.I, dst);
+    if (with_xs) out(g.XS, dst + wimg);
+    if (with_k) out(g.K, dst + 2 * wimg);
+    if (with_a) out(g.A, dst + 3 * wimg);
 }
 
 template <bool HOT>
