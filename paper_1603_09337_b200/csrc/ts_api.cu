@@ -252,7 +252,8 @@ constexpr int kBigThreads = TS_BIG_THREADS;   // threads per CTA of the one-CTA-
 // one fixed flavour: `threads` per CTA, `team` CTAs per image, shared-memory
 // budget `budget_cap` bytes per CTA (<= 0: device maximum)
 int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team,
-                    int threads, long long budget_cap, bool skip_fused = false) {
+                    int threads, long long budget_cap, bool skip_fused = false, bool e4 = false) {
+    if (threads == 256) e4 = true;
     pl.WW = (W + 31) / 32;
     if (H >= (1 << 20) || pl.WW >= (1 << 16))
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");
@@ -283,7 +284,9 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     pl.mwords = (int)size[B_DIRTY];
     size[B_MARK] = r4(((plen + 15) / 16) * 4);
     size[B_LIST] = 2 * plen;   // two compacted re-evaluation lists in dense sweeps
-    size[B_E] = 8 * plen;
+    // E: 8 precedence planes, or 4 (antisymmetry) in the 256-thread and the
+    // generic / team variants (ts_hasf_{8,4}{h256,g}.cu define TS_IMPL_E4)
+    size[B_E] = (e4 ? 4 : 8) * plen;
     size[B_XS] = mode == MODE_HASF ? plen : 0;
     // the fused prep + E-pass (one strip per thread, rows of <= 32 words that
     // tile a warp, r <= 8) keeps the rank slices in registers: no R planes
@@ -325,7 +328,9 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
         (1u << B_I) | (1u << B_D) | (1u << B_C) | (1u << B_DIRTY) | (1u << B_MARK) | (1u << B_CLAIM) | (1u << B_B);
     pl.hot = (pl.mask & hot_mask) == hot_mask;
     if (fused && !pl.hot)   // the fused path runs only with the hot placement: plan the R planes
-        return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, budget_cap, true);
+        return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, budget_cap, true, e4);
+    if (!pl.hot && !e4)     // the generic variant keeps 4 precedence planes: re-plan with them
+        return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, budget_cap, skip_fused, true);
     pl.team = team;
     int blocks = 0;
     if (threads == 256 && !pl.hot) return fail(TS_ERR_UNSUPPORTED, "256-thread flavour needs the hot placement");

@@ -5,6 +5,7 @@
 #define TS_IMPL_THREADS TS_BIG_THREADS
 #define TS_IMPL_MINB 1
 #define TS_IMPL_NS v512
+#define TS_IMPL_E4 1   // 4 precedence planes (antisymmetry), see ts_hasf_impl.cuh
 #include "ts_hasf_impl.cuh"
 
 namespace ts {

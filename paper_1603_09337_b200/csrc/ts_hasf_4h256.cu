@@ -3,6 +3,7 @@
 #define TS_IMPL_THREADS 256
 #define TS_IMPL_MINB 2
 #define TS_IMPL_NS v256
+#define TS_IMPL_E4 1   // 4 precedence planes (antisymmetry), see ts_hasf_impl.cuh
 #include "ts_hasf_impl.cuh"
 
 namespace ts {

@@ -70,6 +70,16 @@ namespace ts {
 namespace TS_IMPL_NS {
 
 constexpr int kThreads = TS_IMPL_THREADS;
+// E4: only the 4 precedence masks towards the raster-earlier neighbours
+// (NW, N, NE, W) are stored, for EVERY word; the other 4 follow by
+// antisymmetry of the (unique) keys from the neighbours' masks (load_e).
+// Half the E footprint: fits shared memory for small images (256-thread
+// variant) and keeps large images' L2 working set down (team variant).
+#ifndef TS_IMPL_E4
+#define TS_IMPL_E4 0
+#endif
+constexpr bool kE4 = TS_IMPL_E4 != 0;
+constexpr int kEWords = kE4 ? 4 : 8;   // E words per bit-plane word
 constexpr int kWarps = kThreads / 32;
 constexpr int kMinBlocks = TS_IMPL_MINB;   // resident images per SM the register budget targets
 
@@ -442,14 +452,35 @@ __device__ __forceinline__ void store_e(const Img &g, int p, const Row3 (&ru)[S]
         cmp_step(lt[1], eq[1], ru[s].c, own);
         cmp_step(lt[2], eq[2], from_east(ru[s].c, ru[s].r), own);
         cmp_step(lt[3], eq[3], from_west(rm[s].l, rm[s].c), own);
-        cmp_step(lt[4], eq[4], from_east(rm[s].c, rm[s].r), own);
-        cmp_step(lt[5], eq[5], from_west(rd[s].l, rd[s].c), own);
-        cmp_step(lt[6], eq[6], rd[s].c, own);
-        cmp_step(lt[7], eq[7], from_east(rd[s].c, rd[s].r), own);
+        if constexpr (!kE4) {
+            cmp_step(lt[4], eq[4], from_east(rm[s].c, rm[s].r), own);
+            cmp_step(lt[5], eq[5], from_west(rd[s].l, rd[s].c), own);
+            cmp_step(lt[6], eq[6], rd[s].c, own);
+            cmp_step(lt[7], eq[7], from_east(rd[s].c, rd[s].r), own);
+        }
     }
-    uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
+    uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * kEWords);
     ep[0] = make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
-    ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
+    if constexpr (!kE4) ep[1] = make_uint4(lt[4], lt[5], lt[6], lt[7]);
+}
+
+// the 8 precedence masks of word p: stored (E8), or (E4) the stored NW, N,
+// NE, W and, by antisymmetry of the unique keys, E(p) = ~W of pixel+1,
+// SW = ~NE of the pixel below-left, S = ~N below, SE = ~NW below-right
+__device__ __forceinline__ void load_e(const Img &g, int p, uint4 &e0, uint4 &e1) {
+    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)p * kEWords);
+    if constexpr (!kE4) {
+        e0 = ep[0];
+        e1 = ep[1];
+    } else {
+        const int S = g.S;
+        e0 = ep[0];
+        const uint4 b = ep[S];                 // word below
+        const uint32_t w_r = g.E[(size_t)(p + 1) * 4 + 3];        // W of the word to the right
+        const uint32_t ne_bl = g.E[(size_t)(p + S - 1) * 4 + 2];  // NE of the word below-left
+        const uint32_t nw_br = g.E[(size_t)(p + S + 1) * 4 + 0];  // NW of the word below-right
+        e1 = make_uint4(~from_east(e0.w, w_r), ~from_west(ne_bl, b.z), ~b.y, ~from_east(b.x, nw_br));
+    }
 }
 
 // E planes from rank slices + the sweep-1 candidates (C, D = C, list).
@@ -480,8 +511,9 @@ __device__ __forceinline__ void epass_ranks(const Img &g, int t, int *counter) {
             if (pre) {
                 c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
                                           from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
-                store_e<S>(g, p, ru, rm, rd);
+                if constexpr (!kE4) store_e<S>(g, p, ru, rm, rd);
             }
+            if constexpr (kE4) store_e<S>(g, p, ru, rm, rd);   // neighbours' masks are read too
             g.C[p] = c;
             g.D[p] = c;
             cnt += c != 0;
@@ -558,8 +590,9 @@ __device__ __forceinline__ void prep_fused(const Img &g, int xmode, bool save_xs
             if (pre) {
                 c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
                                           from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
-                store_e<S>(g, p, ru, rm, rd);
+                if constexpr (!kE4) store_e<S>(g, p, ru, rm, rd);
             }
+            if constexpr (kE4) store_e<S>(g, p, ru, rm, rd);   // neighbours' masks are read too
             g.C[p] = c;
             g.D[p] = c;
             cnt += c != 0;
@@ -588,24 +621,24 @@ __device__ __forceinline__ void epass_prio(const Img &g, const int64_t *prio, in
     const int dx[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
     for_strip(g, [&](int y, int x, int p) {
         uint32_t c = 0;
-        if (~g.B[p]) {
+        if (kE4 || ~g.B[p]) {   // E4: every word's masks (neighbours read them)
             uint32_t e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const int cnt = min(32, g.W - x * 32);
             for (int i = 0; i < cnt; ++i) {
                 const int col = x * 32 + i;
                 const int64_t pv = prio[(size_t)y * g.W + col];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
+                for (int k = 0; k < (kE4 ? 4 : 8); ++k) {
                     const int ny = y + dy[k], nc = col + dx[k];
                     if (ny < 0 || ny >= g.H || nc < 0 || nc >= g.W) continue;
                     const int64_t q = prio[(size_t)ny * g.W + nc];
                     if (q < pv || (q == pv && k < 4)) e[k] |= 1u << i;
                 }
             }
-            uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * 8);
+            uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)p * kEWords);
             ep[0] = make_uint4(e[0], e[1], e[2], e[3]);
-            ep[1] = make_uint4(e[4], e[5], e[6], e[7]);
-            c = cand_word<FG>(g, p, t);
+            if constexpr (!kE4) ep[1] = make_uint4(e[4], e[5], e[6], e[7]);
+            if (~g.B[p]) c = cand_word<FG>(g, p, t);
         }
         g.C[p] = c;
         g.D[p] = c;
@@ -688,11 +721,7 @@ __device__ __forceinline__ bool dense_pass(const Img &g, int pc, int &evals) {
             for (int j = 0; j < kDenseBatch; ++j) {
                 const int q = p + j * g.S;
                 cb[j] = yb + j < y1 ? g.C[q] : 0u;
-                if (cb[j]) {
-                    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
-                    e0b[j] = ep[0];
-                    e1b[j] = ep[1];
-                }
+                if (cb[j]) load_e(g, q, e0b[j], e1b[j]);
             }
 #pragma unroll
             for (int j = 0; j < kDenseBatch; ++j) {
@@ -798,11 +827,7 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, int pc, int &evals) 
         };
         auto fetch = [&](int q, uint32_t &c, uint4 &e0, uint4 &e1) {
             c = g.C[q];
-            if (c) {
-                const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)q * 8);
-                e0 = ep[0];
-                e1 = ep[1];
-            }
+            if (c) load_e(g, q, e0, e1);
         };
         while (y + kDenseBatchL2 <= y1) {
             uint32_t cb[kDenseBatchL2];
@@ -836,9 +861,7 @@ template <int FG>
 __device__ __forceinline__ void load_slot(const Img &g, uint32_t p, Slot &s) {
     s.p = (int)p;
     s.in = nbrs(g.I, g, s.p);
-    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)s.p * 8);
-    s.e0 = ep[0];
-    s.e1 = ep[1];
+    load_e(g, s.p, s.e0, s.e1);
     s.c = g.C[s.p];
     s.d = g.D[s.p];
 }
@@ -1273,7 +1296,7 @@ __device__ __noinline__ TinyOut tiny_sweeps(const View &v, int t, int cur, long 
             const unsigned cm = __ballot_sync(0xffffffffu, c != 0);
             if (c) {
                 g.list[cnt + __popc(cm & lt)] = (uint32_t)q;
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(g.E + (size_t)q * 8));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(g.E + (size_t)q * kEWords));
             }
             cnt += __popc(cm);
             __syncwarp();
@@ -1348,9 +1371,7 @@ struct WordEval {
 __device__ __forceinline__ void load_eval(const Img &g, int p, WordEval &w) {
     w.p = p;
     w.in = nbrs(g.I, g, p);
-    const uint4 *ep = reinterpret_cast<const uint4 *>(g.E + (size_t)p * 8);
-    w.e0 = ep[0];
-    w.e1 = ep[1];
+    load_e(g, p, w.e0, w.e1);
     w.c = g.C[p];
     const uint32_t *u = g.D + p - g.S, *m = g.D + p, *d = g.D + p + g.S;
     w.dn.nw = from_west(u[-1], u[0]);
