@@ -254,6 +254,9 @@ constexpr int kBigThreads = TS_BIG_THREADS;   // threads per CTA of the one-CTA-
 int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg, Plan &pl, int team,
                     int threads, long long budget_cap, bool skip_fused = false, bool e4 = false) {
     if (threads == 256) e4 = true;
+#ifdef TS_IMPL_E4_HOT
+    e4 = true;
+#endif
     pl.WW = (W + 31) / 32;
     if (H >= (1 << 20) || pl.WW >= (1 << 16))
         return fail(TS_ERR_UNSUPPORTED, "image too large for the fused kernel");

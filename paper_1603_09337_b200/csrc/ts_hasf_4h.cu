@@ -5,6 +5,9 @@
 #define TS_IMPL_THREADS TS_BIG_THREADS
 #define TS_IMPL_MINB 1
 #define TS_IMPL_NS v512
+#ifdef TS_IMPL_E4_HOT
+#define TS_IMPL_E4 1   // A-B experiment: 4 precedence planes in the 512-thread hot variant too
+#endif
 #include "ts_hasf_impl.cuh"
 
 namespace ts {
