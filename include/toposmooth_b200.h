@@ -176,8 +176,10 @@ int32_t ts_set_team_size(int32_t ctas);
  * 2048^2 with 4 CTAs each) run as thread-block clusters: hardware cluster
  * barriers instead of the global-atomic team barrier, and the team's control
  * block (queues' counters, list lengths) in the rank-0 CTA's shared memory,
- * reached by the others over distributed shared memory; 0 = cooperative
- * launch with the global control block.  Returns the previous value. */
+ * reached by the others over distributed shared memory; 2 = also teams of
+ * more than 8 CTAs as several clusters with a hierarchical barrier (cluster
+ * barrier + one global arrival per cluster; measured slower on c3); 0 =
+ * cooperative launch with the global control block.  Returns the previous value. */
 int32_t ts_set_cluster_teams(int32_t on);
 
 /* Tuning/testing: force the kernel flavour, 512 threads x 1 CTA/SM or 256 x 2

@@ -440,14 +440,29 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     // teams of 2..8 CTAs run as thread-block clusters (hardware barriers, the
     // control block in DSMEM); larger teams (c3: one image over every SM) use
     // the cooperative launch with a global barrier
-    bool cluster = false;
+    int cluster = 0;   // cluster size of the launch
     int max_teams = pl.per_wave / team;
     if (team >= 2 && team <= 8 && g_cluster_knob.load()) {
         int nc = 0;
         if (hasf_cluster_occupancy(fg, pl.smem_bytes, team, &nc) == cudaSuccess && nc >= 1) {
-            cluster = true;
+            cluster = team;
             max_teams = std::min(max_teams, nc);
         } else {
+            cudaGetLastError();
+        }
+    } else if (team > 8 && g_cluster_knob.load() >= 2 &&
+               team * 1LL * std::min<long long>(n, max_teams) <= pl.per_wave) {
+        // larger teams (c3: one image over all SMs), opt-in: hierarchical barrier
+        // over clusters of 4 (or 2) CTAs when every cluster of the grid fits at
+        // once (measured slower on c3 than the flat barrier: 26.6 vs 25.0 ms)
+        for (int cs : {4, 2}) {
+            if (team % cs) continue;
+            const int teams_ = (int)std::min<long long>(n, max_teams);
+            int nc = 0;
+            if (hasf_cluster_occupancy(fg, pl.smem_bytes, cs, &nc) == cudaSuccess && nc * cs >= teams_ * team) {
+                cluster = cs;
+                break;
+            }
             cudaGetLastError();
         }
     }
@@ -470,7 +485,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
         nseg = seg_count(total_stages, seg_stages, fine);
     const size_t ws_words = (size_t)pl.stride_ws * (team > 1 ? teams : grid);
     const size_t xbuf_words = nseg > 1 ? (size_t)n * 4 * h * pl.WW : 0;   // image, XS, keep, avoid
-    const size_t tctl_bytes = team > 1 && !cluster ? (size_t)teams * kTeamCtlBytes : 0;
+    const size_t tctl_bytes = team > 1 && cluster != team ? (size_t)teams * kTeamCtlBytes : 0;
     const size_t stats_bytes = stats_host ? (size_t)n * kStatFields * sizeof(long long) : 0;
     const size_t prog_bytes = nseg > 1 ? (((size_t)n * sizeof(unsigned) + 63) & ~(size_t)63) : 0;
     const size_t ctrl_bytes = 64 + stats_bytes + prog_bytes + tctl_bytes;
@@ -523,7 +538,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.team = team;
     p.threads = pl.threads;
     p.tctl = tctl_bytes ? (void *)(ctrl + ctrl_bytes - tctl_bytes) : nullptr;
-    p.cluster = cluster ? 1 : 0;
+    p.cluster = cluster;
     p.fused = pl.fused ? 1 : 0;
     p.packed_io = packed_io;
     p.ready = ready;
@@ -1064,7 +1079,7 @@ int32_t ts_set_segment_stages(int32_t stages) { return g_seg_stages.exchange(sta
 
 int32_t ts_set_segment_fine(int32_t stages) { return g_seg_fine.exchange(stages < 0 ? 0 : stages); }
 
-int32_t ts_set_cluster_teams(int32_t on) { return g_cluster_knob.exchange(on ? 1 : 0); }
+int32_t ts_set_cluster_teams(int32_t on) { return g_cluster_knob.exchange(on < 0 ? 0 : (on > 2 ? 2 : on)); }
 
 int32_t ts_set_host_segments(int32_t stages, int32_t fine) {
     g_seg_fine_host.store(fine < 0 ? 0 : fine);

@@ -99,7 +99,8 @@ struct Img {
     int dense_min;       // sweeps with more listed words run in dense mode
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
-    unsigned *bar;       // team barrier [count, generation] (G > 1)
+    int cs;              // thread-block cluster size of the team's launch (1: none; G: the team is one cluster)
+    unsigned *bar;       // team barrier [count, generation] (G > 1, cs < G)
     int *err;
     struct Shared *sh;   // control block: shared memory (G == 1) or global (G > 1)
 };
@@ -127,19 +128,28 @@ __device__ __forceinline__ void team_sync(const Img &g) {
         __syncthreads();
         return;
     }
-    if (g.bar == nullptr) {
+    if (g.cs == g.G) {
         // the team is a thread-block cluster: the hardware cluster barrier,
         // release / acquire at cluster scope (planes written by one CTA of the
         // team are read by the others after it)
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
         return;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // hierarchical (team of several clusters): cluster barrier, then one CTA
+    // per cluster on the global counter (G / cs arrivals instead of G), then
+    // the cluster barrier releases the rest; otherwise every CTA arrives
+    const bool hier = g.cs > 1;
+    if (hier)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
+    const unsigned parts = hier ? (unsigned)(g.G / g.cs) : (unsigned)g.G;
+    const bool leader = threadIdx.x == 0 && (!hier || (g.tid / kThreads) % g.cs == 0);
+    if (leader) {
         volatile unsigned *gen = g.bar + 1;
         const unsigned g0 = *gen;
         __threadfence();
-        if (atomicAdd(g.bar, 1u) == (unsigned)g.G - 1) {
+        if (atomicAdd(g.bar, 1u) == parts - 1) {
             atomicExch(g.bar, 0u);
             __threadfence();
             atomicAdd(g.bar + 1, 1u);
@@ -155,7 +165,10 @@ __device__ __forceinline__ void team_sync(const Img &g) {
         }
         __threadfence();
     }
-    __syncthreads();
+    if (hier)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
 }
 
 struct Nb {
@@ -1056,7 +1069,7 @@ struct View {
     int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, fused, mw;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
-    int G, rank;
+    int G, rank, cs;
     unsigned *bar;
     int *err;
 };
@@ -1099,6 +1112,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.lastmask = v.lastmask;
     // HOT implies a single CTA per image: constants, so team code folds away
     g.G = HOT ? 1 : v.G;
+    g.cs = HOT ? 1 : v.cs;
     g.tid = HOT ? (int)threadIdx.x : v.rank * kThreads + (int)threadIdx.x;
     g.nthr = HOT ? kThreads : v.G * kThreads;
     g.bar = v.bar;
@@ -2053,9 +2067,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     // teams: a global control block (cooperative launch), or -- when the team
     // is a thread-block cluster -- the control block of the team's rank-0 CTA,
     // shared with the others over distributed shared memory (DSMEM)
-    TeamCtl *tc = (G == 1 || p.cluster) ? nullptr : reinterpret_cast<TeamCtl *>(p.tctl) + team;
-    Shared *shp = G == 1 ? &sh_local
-                         : (p.cluster ? reinterpret_cast<Shared *>(dsmem_map(&sh_local, 0)) : &tc->sh);
+    const bool one_cluster = !HOT && G > 1 && p.cluster == G;
+    TeamCtl *tc = (G == 1 || one_cluster) ? nullptr : reinterpret_cast<TeamCtl *>(p.tctl) + team;
+    Shared *shp = G == 1 ? &sh_local : (one_cluster ? reinterpret_cast<Shared *>(dsmem_map(&sh_local, 0)) : &tc->sh);
     View vl;   // built by every thread, published in shared memory: the noinline
                // phases take it by reference (no per-call copy to local memory)
     if constexpr (HOT) {
@@ -2097,13 +2111,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     vl.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
     vl.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;
     vl.G = G;
+    vl.cs = G > 1 && p.cluster > 1 ? p.cluster : 1;
     vl.rank = rank;
     vl.bar = tc ? tc->bar : nullptr;
     vl.err = p.err;
     __shared__ View v_shared;
     if (threadIdx.x == 0) v_shared = vl;
     __syncthreads();
-    if (!HOT && p.cluster) {   // rank 0's control block: zeroed, and every CTA of the cluster running
+    if (one_cluster) {   // rank 0's control block: zeroed, and every CTA of the cluster running
         if (rank == 0 && threadIdx.x == 0) sh_local = Shared{};
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
@@ -2269,7 +2284,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         }
     }
     // cluster teams: no CTA leaves while another may still read rank 0's control block
-    if (!HOT && p.cluster)
+    if (one_cluster)
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
@@ -2291,19 +2306,21 @@ cudaError_t raise_smem_limit_once(const void *fn, std::mutex &mu, bool (&done)[6
         cudaError_t e = raise_smem_limit_once(fn, g_attr_mu_##SUFFIX, g_attr_done_##SUFFIX);                   \
         if (e != cudaSuccess) return e;                                                                         \
         void *args[] = {(void *)&p};                                                                            \
-        if (p.team > 1 && p.cluster) {                                                                          \
+        if (p.team > 1 && p.cluster > 1) {   /* clusters of p.cluster CTAs; several per team: cooperative */   \
             cudaLaunchConfig_t cfg{};                                                                           \
-            cudaLaunchAttribute at[1];                                                                          \
+            cudaLaunchAttribute at[2];                                                                          \
             at[0].id = cudaLaunchAttributeClusterDimension;                                                     \
-            at[0].val.clusterDim.x = (unsigned)p.team;                                                          \
+            at[0].val.clusterDim.x = (unsigned)p.cluster;                                                       \
             at[0].val.clusterDim.y = 1;                                                                         \
             at[0].val.clusterDim.z = 1;                                                                         \
+            at[1].id = cudaLaunchAttributeCooperative;                                                          \
+            at[1].val.cooperative = 1;                                                                          \
             cfg.gridDim = dim3(grid);                                                                           \
             cfg.blockDim = dim3(kThreads);                                                                      \
             cfg.dynamicSmemBytes = smem_bytes;                                                                  \
             cfg.stream = stream;                                                                                \
             cfg.attrs = at;                                                                                     \
-            cfg.numAttrs = 1;                                                                                   \
+            cfg.numAttrs = p.cluster < p.team ? 2 : 1;                                                          \
             return cudaLaunchKernelExC(&cfg, fn, args);                                                         \
         }                                                                                                       \
         if (p.team > 1)                                                                                         \

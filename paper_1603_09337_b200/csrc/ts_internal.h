@@ -99,7 +99,9 @@ struct KParams {
     int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
     int threads;            // threads per CTA of the variant (512, or 256 = two CTAs per SM)
     void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1, not a cluster)
-    int cluster;            // 1: each team is a thread-block cluster (control block in rank 0's smem, cluster barriers)
+    int cluster;            // thread-block cluster size of the launch (0/1 none); == team: each team is one
+                            // cluster (control block in rank 0's smem, cluster barriers); < team: hierarchical
+                            // team barrier (cluster barrier + one global arrival per cluster)
     int r_first, r_last, do_cut, do_fill;
     int mode;
     long long max_sweeps;   // < 0: unbounded

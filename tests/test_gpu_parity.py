@@ -236,12 +236,14 @@ def team_knob():
     lib.ts_set_team_size(0)
 
 
-@pytest.mark.parametrize("team,cluster", [(2, 1), (3, 1), (5, 1), (8, 1), (2, 0), (3, 0), (5, 0)])
+@pytest.mark.parametrize("team,cluster", [(2, 1), (3, 1), (5, 1), (8, 1), (12, 2), (10, 2), (2, 0), (3, 0), (5, 0),
+                                          (12, 0)])
 def test_team_mode_vs_oracle(team_knob, team, cluster):
     """Teams of CTAs sharing one image through L2 (the large-image path),
     forced on small images so the oracle can check them: as thread-block
-    clusters (hardware barrier, control block over DSMEM) and as a
-    cooperative launch with the global barrier."""
+    clusters (hardware barrier, control block over DSMEM), as several
+    clusters per team (teams > 8: hierarchical barrier) and as a cooperative
+    launch with the global barrier."""
     team_knob.ts_set_team_size(team)
     old_cluster = team_knob.ts_set_cluster_teams(cluster)
     try:
