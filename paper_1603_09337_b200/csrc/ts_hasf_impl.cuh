@@ -80,6 +80,9 @@ constexpr int kThreads = TS_IMPL_THREADS;
 #endif
 constexpr bool kE4 = TS_IMPL_E4 != 0;
 constexpr int kEWords = kE4 ? 4 : 8;   // E words per bit-plane word
+#ifndef TS_PREP_U4
+#define TS_PREP_U4 1   // fused prep: 4 comparators per word, lower masks by antisymmetry (E8 variants)
+#endif
 constexpr int kWarps = kThreads / 32;
 constexpr int kMinBlocks = TS_IMPL_MINB;   // resident images per SM the register budget targets
 
@@ -591,6 +594,84 @@ __device__ __forceinline__ void prep_fused(const Img &g, int xmode, bool save_xs
     const int steps = g.hb;   // warp-uniform trip count (shorter strips idle)
     int p = pidx(g, y0, x);
     Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
+#if TS_PREP_U4
+    // E8 storage from 4 comparators per word: at row y the masks towards the
+    // upper neighbours U(y) = {NW, N, NE, W} (every word, all lanes); row
+    // y-1's lower four follow by antisymmetry of the unique keys and are
+    // stored one step late: S = ~N(y), SW = ~NE(y) of pixel-1 (lane-1 at bit
+    // 0), SE = ~NW(y) of pixel+1, E = ~W of pixel+1 (lane+1 at bit 31; pads
+    // at row ends: those neighbours' decisions are 0)
+    if constexpr (!kE4) {
+        auto upper = [&]() -> uint4 {
+            uint32_t lt[4], eq[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                lt[k] = 0;
+                eq[k] = ~0u;
+            }
+#pragma unroll
+            for (int s = S - 1; s >= 0; --s) {
+                const uint32_t own = rm[s].c;
+                cmp_step(lt[0], eq[0], from_west(ru[s].l, ru[s].c), own);
+                cmp_step(lt[1], eq[1], ru[s].c, own);
+                cmp_step(lt[2], eq[2], from_east(ru[s].c, ru[s].r), own);
+                cmp_step(lt[3], eq[3], from_west(rm[s].l, rm[s].c), own);
+            }
+            return make_uint4(lt[0] | eq[0], lt[1] | eq[1], lt[2] | eq[2], lt[3] | eq[3]);
+        };
+        uint4 uprev = make_uint4(0, 0, 0, 0);
+        uint32_t eprev = 0, cprev = 0;
+        int pprev = 0;
+        auto finish = [&](const uint4 &u) {   // row y-1's masks, given U(y); returns E of row y
+            const uint32_t w_r = __shfl_down_sync(0xffffffffu, u.w, 1);
+            const uint32_t ne_l = __shfl_up_sync(0xffffffffu, u.z, 1);
+            const uint32_t nw_r = __shfl_down_sync(0xffffffffu, u.x, 1);
+            if (cprev) {   // (E is read only for words with unblocked target pixels, see below)
+                uint4 *ep = reinterpret_cast<uint4 *>(g.E + (size_t)pprev * 8);
+                ep[0] = uprev;
+                ep[1] = make_uint4(eprev, ~from_west(ne_l, u.z), ~u.y, ~from_east(u.x, nw_r));
+            }
+            return ~from_east(u.w, w_r);
+        };
+        for (int j = 0; j < steps; ++j, p += g.S) {
+            const int y = y0 + j;
+            row(y + 1, rd, bd);
+            const uint4 u = upper();
+            const uint32_t e_here = finish(u);
+            cprev = 0;
+            if (y < y1) {
+                const Row3 id = row3(g.I, p + g.S);
+                const uint32_t pre = (t ? im.c : ~im.c) & ~bm;
+                uint32_t c = 0;
+                if (pre)
+                    c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r),
+                                              from_west(im.l, im.c), from_east(im.c, im.r), from_west(id.l, id.c),
+                                              id.c, from_east(id.c, id.r));
+                g.C[p] = c;
+                g.D[p] = c;
+                cnt += c != 0;
+                cprev = pre;   // any later sweep's candidates lie inside pre
+                pprev = p;
+                iu = im;
+                im = id;
+            }
+            uprev = u;
+            eprev = e_here;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                ru[s] = rm[s];
+                rm[s] = rd[s];
+            }
+            bu = bm;
+            bm = bd;
+        }
+        finish(upper());   // the strip's last row, from the row below it
+        (void)lane;
+        (void)bu;
+        add_count(cnt, counter);
+        return;
+    }
+#endif
     for (int j = 0; j < steps; ++j, p += g.S) {
         const int y = y0 + j;
         row(y + 1, rd, bd);
