@@ -1,6 +1,8 @@
-"""Randomised parity stress (GPU): many random shapes / densities / radii /
-adjacencies / constraints through hasf_batch (and the host entry), each
-checked bit-exact against the oracle.  Not part of the test suite (minutes).
+"""Randomised parity stress (GPU): many random shapes / densities / radii
+(incl. 17..20, the stage path) / adjacencies / constraints through
+hasf_batch, the host entry and the P4 entry, under random kernel flavours,
+team sizes (clusters, hierarchical, cooperative) and forced segmentation,
+each checked bit-exact against the oracle.  Not part of the test suite.
     python tools/stress_parity.py [--cases 300] [--seed 0]"""
 import argparse
 import os
@@ -50,12 +52,21 @@ def main():
         if rng.random() < 0.3:
             keep = (imgs & (rng.random(imgs.shape) < 0.03)).astype(np.uint8)
             avoid = ((rng.random(imgs.shape) < 0.03) & (imgs == 0)).astype(np.uint8)
-        knobs = {"threads": int(rng.choice([0, 256, 512])), "team": int(rng.choice([0, 0, 0, 2, 3])),
-                 "fused": int(rng.choice([0, 1, 1])), "dense": int(rng.choice([2, 4, 8]))}
+        if rng.random() < 0.03:   # radii above the fused kernel: the stage path
+            r = int(rng.integers(17, 21))
+        knobs = {"threads": int(rng.choice([0, 256, 512])), "team": int(rng.choice([0, 0, 0, 2, 3, 5, 8, 12])),
+                 "fused": int(rng.choice([0, 1, 1])), "dense": int(rng.choice([2, 4, 8])),
+                 "cluster": int(rng.choice([0, 1, 1, 2])), "seg_force": int(rng.random() < 0.3),
+                 "seg": int(rng.choice([1, 2, 4, 8])), "fine": int(rng.choice([0, 1, 2, 3]))}
         lib.ts_set_cta_threads(knobs["threads"])
         lib.ts_set_team_size(knobs["team"])
         lib.ts_set_fused_prep(knobs["fused"])
         lib.ts_set_dense_divisor(knobs["dense"])
+        lib.ts_set_cluster_teams(knobs["cluster"])
+        lib.ts_set_segment_force(knobs["seg_force"])
+        lib.ts_set_segment_stages(knobs["seg"])
+        lib.ts_set_segment_fine(knobs["fine"])
+        lib.ts_set_host_segments(knobs["seg"], knobs["fine"])
         adj = P.ADJ_84 if fg == 8 else P.ADJ_48
         want = O.hasf_batch(imgs, r, fg, keep=keep, avoid=avoid, threads=8)
         try:
@@ -65,17 +76,26 @@ def main():
                 continue
             raise
         ok = np.array_equal(got, want)
-        if keep is None and knobs["team"] == 0:
+        if knobs["team"] == 0:   # the host entry (packed / uint8 streaming / chunked), constraints too
             lib.ts_set_host_streaming(int(rng.choice([0, 1, 2])))
             hout = np.zeros_like(imgs)
-            _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, hout.ctypes.data, n, h, w, r, fg, None, None, None))
+            kp = None if keep is None else keep.ctypes.data
+            ap_ = None if avoid is None else avoid.ctypes.data
+            _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, hout.ctypes.data, n, h, w, r, fg, kp, ap_, None))
             ok = ok and np.array_equal(hout, want)
+        if rng.random() < 0.15:   # P4 rasters through the device bit rows
+            pk = None if keep is None else np.packbits(keep, axis=2)
+            pa = None if avoid is None else np.packbits(avoid, axis=2)
+            got4 = P.hasf_p4(np.packbits(imgs, axis=2), w, r, adj, keep=pk, avoid=pa)
+            ok = ok and np.array_equal(np.unpackbits(got4, axis=2)[:, :, :w], want)
         if not ok:
             bad += 1
             print("MISMATCH", i, dict(h=h, w=w, n=n, fg=fg, r=r, constraints=keep is not None, **knobs), flush=True)
     for f, v in (("ts_set_cta_threads", 0), ("ts_set_team_size", 0), ("ts_set_fused_prep", 1),
-                 ("ts_set_dense_divisor", 4), ("ts_set_host_streaming", 1)):
+                 ("ts_set_dense_divisor", 4), ("ts_set_host_streaming", 1), ("ts_set_cluster_teams", 1),
+                 ("ts_set_segment_force", 0), ("ts_set_segment_stages", 8), ("ts_set_segment_fine", 2)):
         getattr(lib, f)(v)
+    lib.ts_set_host_segments(8, 0)
     print(f"stress: {a.cases} cases, {bad} mismatches")
     sys.exit(1 if bad else 0)
 
