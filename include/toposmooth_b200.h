@@ -183,7 +183,9 @@ int32_t ts_set_team_size(int32_t ctas);
 int32_t ts_set_cluster_teams(int32_t on);
 
 /* Tuning/testing: force the kernel flavour, 512 threads x 1 CTA/SM or 256 x 2
- * (0 = automatic: 256 x 2 when the hot planes fit half an SM).  Returns the previous value. */
+ * (0 = automatic: 256 x 2 when the hot planes fit half an SM; 1024 threads per
+ * CTA for the cluster teams of large images); 1024 forces 1024-thread CTAs for
+ * every team, 512 forces 512-thread teams.  Returns the previous value. */
 int32_t ts_set_cta_threads(int32_t threads);
 
 /* Tuning / A-B of ts_hasf_batch_host: 1 (default) = the images are bit-packed

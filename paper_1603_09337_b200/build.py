@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libtoposmooth_b200.so")
 SOURCES = ["ts_hasf_8h.cu", "ts_hasf_4h.cu", "ts_hasf_8g.cu", "ts_hasf_4g.cu", "ts_hasf_8h256.cu",
-           "ts_hasf_4h256.cu", "ts_hasf.cu", "ts_edt.cu", "ts_ccl.cu", "ts_p4.cu", "ts_api.cu", "ts_hostpack.cpp"]
+           "ts_hasf_4h256.cu", "ts_hasf_8g1024.cu", "ts_hasf_4g1024.cu", "ts_hasf.cu", "ts_edt.cu", "ts_ccl.cu", "ts_p4.cu", "ts_api.cu", "ts_hostpack.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]

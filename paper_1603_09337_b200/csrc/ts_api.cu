@@ -25,7 +25,7 @@
 namespace ts {
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream);
 cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm);
-cudaError_t hasf_cluster_occupancy(int fg, size_t smem_bytes, int team, int *clusters);
+cudaError_t hasf_cluster_occupancy(int fg, int threads, size_t smem_bytes, int team, int *clusters);
 cudaError_t launch_edt_phase1(const uint8_t *pix, long long *g, int n, int H, int W, int invert, long long inf,
                               cudaStream_t st);
 cudaError_t launch_edt(const uint8_t *pix, const long long *g64, void *out, int *scratch, int n, int H, int W,
@@ -303,7 +303,7 @@ int make_plan_fixed(int H, int W, int r_last, int mode, bool has_k, bool has_a, 
     int sms = 0, optin = 0, per_sm = 0;
     int rc = device_props(&sms, &optin, &per_sm);
     if (rc) return rc;
-    long long budget = optin - 512;   // static Shared block of the kernel
+    long long budget = optin - kStaticSmemReserve;   // static Shared block, View, epoch of the kernel
     if (budget_cap > 0 && budget_cap < budget) budget = budget_cap;
     const long long knob = g_smem_budget.load();
     if (knob > 0 && knob < budget) budget = knob;
@@ -353,7 +353,7 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         int rc = device_props(&sms, &optin, &per_sm);
         if (rc) return rc;
         Plan p2;
-        const long long half = per_sm / 2 - 1024 - 512;
+        const long long half = per_sm / 2 - 1024 - kStaticSmemReserve;
         rc = make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, p2, 1, 256, half);
         // (measured: two images per SM pay off only when each thread walks a
         // single strip; with two strips per thread c1 ran 10% slower)
@@ -363,7 +363,12 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
         }
         if (knob == 256) return rc ? rc : fail(TS_ERR_UNSUPPORTED, "256-thread flavour does not fit");
     }
-    return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, kBigThreads, 0);
+    // cluster teams (2..8 CTAs, planes in L2) are latency bound: 1024 threads
+    // per CTA (64 registers) hide more of it; the cooperative teams of very
+    // large images are barrier bound and keep 512
+    int threads = kBigThreads;
+    if (team >= 2 && ((team <= 8 && g_cluster_knob.load() && knob != kBigThreads) || knob == 1024)) threads = 1024;
+    return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, 0);
 }
 
 const char *err_message(int code, int mode) {
@@ -444,7 +449,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     int max_teams = pl.per_wave / team;
     if (team >= 2 && team <= 8 && g_cluster_knob.load()) {
         int nc = 0;
-        if (hasf_cluster_occupancy(fg, pl.smem_bytes, team, &nc) == cudaSuccess && nc >= 1) {
+        if (hasf_cluster_occupancy(fg, pl.threads, pl.smem_bytes, team, &nc) == cudaSuccess && nc >= 1) {
             cluster = team;
             max_teams = std::min(max_teams, nc);
         } else {
@@ -459,7 +464,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
             if (team % cs) continue;
             const int teams_ = (int)std::min<long long>(n, max_teams);
             int nc = 0;
-            if (hasf_cluster_occupancy(fg, pl.smem_bytes, cs, &nc) == cudaSuccess && nc * cs >= teams_ * team) {
+            if (hasf_cluster_occupancy(fg, pl.threads, pl.smem_bytes, cs, &nc) == cudaSuccess && nc * cs >= teams_ * team) {
                 cluster = cs;
                 break;
             }
@@ -697,7 +702,7 @@ int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 2 
 int32_t ts_set_team_size(int32_t ctas) { return g_team_knob.exchange(ctas < 0 ? 0 : ctas); }
 
 int32_t ts_set_cta_threads(int32_t threads) {
-    return g_threads_knob.exchange(threads == 256 || threads == kBigThreads ? threads : 0);
+    return g_threads_knob.exchange(threads == 256 || threads == kBigThreads || threads == 1024 ? threads : 0);
 }
 
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {

@@ -103,7 +103,8 @@ struct Img {
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
     int cs;              // thread-block cluster size of the team's launch (1: none; G: the team is one cluster)
-    unsigned *bar;       // team barrier [count, generation] (G > 1, cs < G)
+    unsigned *bar;       // team barrier: monotonic arrival counter (G > 1, cs < G)
+    unsigned *epoch;     // this CTA's count of team barriers (shared memory)
     int *err;
     struct Shared *sh;   // control block: shared memory (G == 1) or global (G > 1)
 };
@@ -120,12 +121,16 @@ __device__ __forceinline__ void *dsmem_map(void *p, unsigned rank) {
     return r;
 }
 
-// Barrier over the G CTAs of a team (co-resident: cooperative launch).  Thread 0
-// of each CTA arrives on a global counter; the last one resets it and bumps the
-// generation.  The gpu-scope fences order the CTA's writes before the arrival
-// and (CCTL.IVALL) drop stale L1 lines after the release, so plane data written
-// by other CTAs is read from L2.  A spin bound turns a lost CTA into an error
-// instead of a hang.
+// Barrier over the G CTAs of a team (co-resident: cooperative launch).  One
+// monotonic arrival counter per team: barrier number k (counted per CTA in
+// *g.epoch; every CTA of a team executes the same barriers) completes when the
+// counter reaches k * arrivals.  Thread 0 of each CTA arrives with a
+// fire-and-forget red.release (the CTA's writes, ordered by the __syncthreads
+// before it, are visible at gpu scope first) and polls with ld.acquire (which
+// drops this SM's stale L1 lines, so plane data written by other CTAs is read
+// from L2): one L2 round trip on the critical path instead of four (generation
+// read, arrival atomic with return, counter reset, generation bump).  A spin
+// bound turns a lost CTA into an error instead of a hang.
 __device__ __forceinline__ void team_sync(const Img &g) {
     if (g.G == 1) {
         __syncthreads();
@@ -148,25 +153,21 @@ __device__ __forceinline__ void team_sync(const Img &g) {
         __syncthreads();
     const unsigned parts = hier ? (unsigned)(g.G / g.cs) : (unsigned)g.G;
     const bool leader = threadIdx.x == 0 && (!hier || (g.tid / kThreads) % g.cs == 0);
-    if (leader) {
-        volatile unsigned *gen = g.bar + 1;
-        const unsigned g0 = *gen;
-        __threadfence();
-        if (atomicAdd(g.bar, 1u) == parts - 1) {
-            atomicExch(g.bar, 0u);
-            __threadfence();
-            atomicAdd(g.bar + 1, 1u);
-        } else {
+    if (threadIdx.x == 0) {
+        const unsigned target = (*g.epoch += 1u) * parts;   // every CTA counts, leaders arrive
+        if (leader) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.bar) : "memory");
             long long spins = 0;
-            while (*gen == g0) {
-                __nanosleep(64);
-                if (++spins > (1LL << 26)) {   // ~ seconds
+            while (true) {
+                unsigned c;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(g.bar) : "memory");
+                if ((int)(c - target) >= 0) break;
+                if (++spins > (1LL << 27)) {   // ~ seconds
                     set_err(g.err, ERR_TEAM_TIMEOUT);
                     break;
                 }
             }
         }
-        __threadfence();
     }
     if (hier)
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1152,6 +1153,7 @@ struct View {
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank, cs;
     unsigned *bar;
+    unsigned *epoch;
     int *err;
 };
 
@@ -1197,6 +1199,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.tid = HOT ? (int)threadIdx.x : v.rank * kThreads + (int)threadIdx.x;
     g.nthr = HOT ? kThreads : v.G * kThreads;
     g.bar = v.bar;
+    g.epoch = v.epoch;
     g.err = v.err;
     g.sh = g.G == 1 ? reinterpret_cast<Shared *>(__cvta_shared_to_generic((size_t)v.sh))
                     : reinterpret_cast<Shared *>(v.sh);
@@ -2195,9 +2198,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     vl.cs = G > 1 && p.cluster > 1 ? p.cluster : 1;
     vl.rank = rank;
     vl.bar = tc ? tc->bar : nullptr;
+    __shared__ unsigned epoch_local;
+    vl.epoch = &epoch_local;
     vl.err = p.err;
     __shared__ View v_shared;
-    if (threadIdx.x == 0) v_shared = vl;
+    static_assert(sizeof(Shared) + sizeof(View) + 16 <= kStaticSmemReserve, "kStaticSmemReserve too small");
+    if (threadIdx.x == 0) {
+        v_shared = vl;
+        epoch_local = 0;
+    }
     __syncthreads();
     if (one_cluster) {   // rank 0's control block: zeroed, and every CTA of the cluster running
         if (rank == 0 && threadIdx.x == 0) sh_local = Shared{};

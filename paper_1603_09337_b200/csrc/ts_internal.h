@@ -29,6 +29,10 @@ constexpr int kMaxSegs = 64;
 // input ready, loaded, its stages done, its result stored, finished
 constexpr int kTraceFields = 7;
 
+// static shared memory of the fused kernel (control block, View, barrier
+// epoch) that the host planner leaves out of the dynamic budget
+constexpr int kStaticSmemReserve = 768;
+
 // bytes reserved per team control block (teams of > 1 CTA per image)
 constexpr int kTeamCtlBytes = 8192;
 
