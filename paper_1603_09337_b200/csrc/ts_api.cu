@@ -367,7 +367,7 @@ int make_plan(int H, int W, int r_last, int mode, bool has_k, bool has_a, int fg
     // per CTA (64 registers) hide more of it; the cooperative teams of very
     // large images are barrier bound and keep 512
     int threads = kBigThreads;
-    if (team >= 2 && ((team <= 8 && g_cluster_knob.load() && knob != kBigThreads) || knob == 1024)) threads = 1024;
+    if (team >= 2 && ((team <= 8 && g_cluster_knob.load() && knob != kBigThreads) || knob == kWideThreads)) threads = kWideThreads;
     return make_plan_fixed(H, W, r_last, mode, has_k, has_a, fg, pl, team, threads, 0);
 }
 
@@ -702,7 +702,8 @@ int32_t ts_set_dense_divisor(int32_t div) { return g_dense_div.exchange(div < 2 
 int32_t ts_set_team_size(int32_t ctas) { return g_team_knob.exchange(ctas < 0 ? 0 : ctas); }
 
 int32_t ts_set_cta_threads(int32_t threads) {
-    return g_threads_knob.exchange(threads == 256 || threads == kBigThreads || threads == 1024 ? threads : 0);
+    if (threads == 1024) threads = kWideThreads;   // "the wide flavour"
+    return g_threads_knob.exchange(threads == 256 || threads == kBigThreads || threads == kWideThreads ? threads : 0);
 }
 
 int ts_hasf_plan(int32_t h, int32_t w, int32_t r_max, int32_t has_keep, int32_t has_avoid, int64_t *info5) {

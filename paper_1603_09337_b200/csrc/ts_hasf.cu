@@ -39,7 +39,7 @@ cudaError_t raise_smem_limit_once(const void *fn, std::mutex &mu, bool (&done)[6
 // threads: 512 (any placement), 256 (hot placement only, two CTAs per SM) or
 // 1024 (global placement only: cluster teams)
 cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, cudaStream_t stream) {
-    if (p.threads == 1024 && !p.hot) {
+    if (p.threads == kWideThreads && !p.hot) {
         return fg == 8 ? launch_hasf_8g1024(p, grid, smem_bytes, stream) : launch_hasf_4g1024(p, grid, smem_bytes, stream);
     }
     if (p.threads == 256 && p.hot) {
@@ -51,13 +51,13 @@ cudaError_t launch_hasf(const KParams &p, int fg, int grid, size_t smem_bytes, c
 
 // co-resident clusters of `team` CTAs of the global-placement variant
 cudaError_t hasf_cluster_occupancy(int fg, int threads, size_t smem_bytes, int team, int *clusters) {
-    if (threads == 1024)
+    if (threads == kWideThreads)
         return fg == 8 ? clusters_hasf_8g1024(smem_bytes, team, clusters) : clusters_hasf_4g1024(smem_bytes, team, clusters);
     return fg == 8 ? clusters_hasf_8g(smem_bytes, team, clusters) : clusters_hasf_4g(smem_bytes, team, clusters);
 }
 
 cudaError_t hasf_occupancy(int fg, bool hot, int threads, size_t smem_bytes, int *blocks_per_sm) {
-    if (threads == 1024) {
+    if (threads == kWideThreads) {
         if (hot) return cudaErrorInvalidValue;
         return fg == 8 ? occupancy_hasf_8g1024(smem_bytes, blocks_per_sm) : occupancy_hasf_4g1024(smem_bytes, blocks_per_sm);
     }

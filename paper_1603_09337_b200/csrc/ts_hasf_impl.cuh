@@ -796,7 +796,15 @@ constexpr int kDenseBatch = TS_DENSE_BATCH;
 #ifndef TS_DENSE_BATCH_L2
 #define TS_DENSE_BATCH_L2 2
 #endif
-constexpr int kDenseBatchL2 = TS_DENSE_BATCH_L2;   // rows whose C / E loads are in flight together (L2 planes)
+#ifndef TS_DENSE_PIPE
+#define TS_DENSE_PIPE 1
+#endif
+constexpr bool kDensePipe = TS_DENSE_PIPE != 0;   // software-pipelined strip walk over L2 planes
+constexpr int kDenseBatchL2 = TS_DENSE_BATCH_L2;
+#ifndef TS_STREAM_BATCH
+#define TS_STREAM_BATCH 4
+#endif
+constexpr int kStreamBatch = TS_STREAM_BATCH;   // rows per load batch of the streaming passes over L2 / DRAM planes   // rows whose C / E loads are in flight together (L2 planes)
 
 
 template <int FG>
@@ -872,9 +880,10 @@ __device__ __forceinline__ bool dense_pass(const Img &g, int pc, int &evals) {
     return ch;
 }
 
-// variant for the L2-resident planes (generic / team kernel): measured faster there
+// L2-resident planes, plain batches (the 1024-thread variant: 64 registers
+// per thread leave no room for the pipelined walk's prefetched rows)
 template <int FG>
-__device__ __forceinline__ bool dense_pass_l2(const Img &g, int pc, int &evals) {
+__device__ __forceinline__ bool dense_pass_l2_plain(const Img &g, int pc, int &evals) {
     bool ch = false;
     const uint8_t next = (uint8_t)(pc + 1);
     auto strip = [&](int x, int y0, int y1, int) {
@@ -924,19 +933,105 @@ __device__ __forceinline__ bool dense_pass_l2(const Img &g, int pc, int &evals) 
             c = g.C[q];
             if (c) load_e(g, q, e0, e1);
         };
-        while (y + kDenseBatchL2 <= y1) {
-            uint32_t cb[kDenseBatchL2];
-            uint4 e0b[kDenseBatchL2], e1b[kDenseBatchL2];
+        while (y + 2 <= y1) {
+            uint32_t cb[2];
+            uint4 e0b[2], e1b[2];
 #pragma unroll
-            for (int j = 0; j < kDenseBatchL2; ++j) fetch(p + j * g.S, cb[j], e0b[j], e1b[j]);
+            for (int j = 0; j < 2; ++j) fetch(p + j * g.S, cb[j], e0b[j], e1b[j]);
 #pragma unroll
-            for (int j = 0; j < kDenseBatchL2; ++j) step(cb[j], e0b[j], e1b[j]);
+            for (int j = 0; j < 2; ++j) step(cb[j], e0b[j], e1b[j]);
         }
         while (y < y1) {
             uint32_t c;
             uint4 e0, e1;
             fetch(p, c, e0, e1);
             step(c, e0, e1);
+        }
+    };
+    walk_strips(g, strip);
+    return ch;
+}
+
+// variant for the L2-resident planes (generic / team kernel).  Software
+// pipelined over batches of kDenseBatchL2 rows: a batch's candidate words are
+// requested one batch ahead, so its E masks (needed only where candidates
+// exist), the image / decision rows below it and the next batch's candidates
+// are all in flight together -- one L2 / DRAM latency per batch instead of
+// three dependent ones per row.  Prefetched decisions of the neighbouring
+// columns may be stale: any evaluation order reaches the fixpoint, and every
+// later change stamps the words it affects.
+template <int FG>
+__device__ __forceinline__ bool dense_pass_l2(const Img &g, int pc, int &evals) {
+    bool ch = false;
+    const uint8_t next = (uint8_t)(pc + 1);
+    constexpr int KB = kDenseBatchL2;
+    auto strip = [&](int x, int y0, int y1, int) {
+        if (y0 >= y1) return;
+        int p = pidx(g, y0, x);
+        const int S = g.S;
+        Row3 iu = row3(g.I, p - S), im = row3(g.I, p);
+        Row3 du = row3(g.D, p - S), dm = row3(g.D, p);
+        uint32_t cn[KB];
+#pragma unroll
+        for (int j = 0; j < KB; ++j) cn[j] = y0 + j < y1 ? g.C[p + j * S] : 0u;
+        for (int yb = y0; yb < y1; yb += KB) {
+            uint32_t cb[KB];
+            uint4 e0b[KB], e1b[KB];
+            Row3 idb[KB], ddb[KB];
+#pragma unroll
+            for (int j = 0; j < KB; ++j) {
+                cb[j] = cn[j];
+                if (cb[j]) load_e(g, p + j * S, e0b[j], e1b[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < KB; ++j) {
+                if (yb + j < y1) {
+                    idb[j] = row3(g.I, p + (j + 1) * S);
+                    ddb[j] = row3(g.D, p + (j + 1) * S);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < KB; ++j) cn[j] = yb + KB + j < y1 ? g.C[p + (KB + j) * S] : 0u;
+#pragma unroll
+            for (int j = 0; j < KB; ++j) {
+                if (yb + j >= y1) break;
+                const Row3 id = idb[j], dd = ddb[j];
+                const uint32_t c = cb[j];
+                if (c) {
+                    const uint4 e0 = e0b[j], e1 = e1b[j];
+                    Nb in, dn;
+                    in.nw = from_west(iu.l, iu.c);
+                    in.n = iu.c;
+                    in.ne = from_east(iu.c, iu.r);
+                    in.w = from_west(im.l, im.c);
+                    in.e = from_east(im.c, im.r);
+                    in.sw = from_west(id.l, id.c);
+                    in.s = id.c;
+                    in.se = from_east(id.c, id.r);
+                    dn.nw = from_west(du.l, du.c);
+                    dn.n = du.c;
+                    dn.ne = from_east(du.c, du.r);
+                    dn.w = from_west(dm.l, dm.c);
+                    dn.e = from_east(dm.c, dm.r);
+                    dn.sw = from_west(dd.l, dd.c);
+                    dn.s = dd.c;
+                    dn.se = from_east(dd.c, dd.r);
+                    const uint32_t nd = decide<FG>(c, in, dn, e0, e1);
+                    ++evals;
+                    if (nd != dm.c) {
+                        const uint32_t chg = nd ^ dm.c;
+                        g.D[p] = nd;
+                        dm.c = nd;
+                        stamp_chg(g, p, chg, e0, e1, next, true);
+                        ch = true;
+                    }
+                }
+                iu = im;
+                im = id;
+                du = dm;
+                dm = dd;
+                p += S;
+            }
         }
     };
     walk_strips(g, strip);
@@ -1050,46 +1145,42 @@ __device__ __forceinline__ void rebuild_compact(const Img &g, int t, uint32_t *d
     }
 }
 
-// re-examine every dirty word (warp per 32-word bitmap group, lane = word)
-template <int FG>
-__device__ __forceinline__ void rebuild_sparse(const Img &g, int t, int *counter) {
-    const int lane = threadIdx.x & 31, warp = g.tid >> 5;
-    const int nq = (g.plen + 31) >> 5;
-    for (int q = warp; q < nq; q += g.nthr >> 5) {
-        const uint32_t bits = g.dirty[q];
-        if (bits == 0) continue;   // warp-uniform
-        __syncwarp();
-        if (lane == 0) g.dirty[q] = 0;
-        const int p = q * 32 + lane;
-        uint32_t c = 0;
-        if ((bits >> lane) & 1u) {
-            c = cand_word<FG>(g, p, t);
-            g.C[p] = c;
-            g.D[p] = c;
-        }
-        append(c != 0, (uint32_t)p, g.list, counter);
-    }
-}
-
-// recompute the candidates of every word (after a dense sweep)
-template <int FG>
+// recompute the candidates of every word (after a dense sweep).  KB rows'
+// loads (I rows, B) are issued together: one memory latency per batch when the
+// planes live in L2 / DRAM (KB = 1 in shared memory)
+template <int FG, int KB>
 __device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter) {
     int cnt = 0;
     auto strip = [&](int x, int y0, int y1) {
         int p = pidx(g, y0, x);
         Row3 iu = row3(g.I, p - g.S), im = row3(g.I, p);
-        for (int y = y0; y < y1; ++y, p += g.S) {
-            const Row3 id = row3(g.I, p + g.S);
-            const uint32_t pre = (t ? im.c : ~im.c) & ~g.B[p];
-            uint32_t c = 0;
-            if (pre)
-                c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r), from_west(im.l, im.c),
-                                          from_east(im.c, im.r), from_west(id.l, id.c), id.c, from_east(id.c, id.r));
-            g.C[p] = c;
-            g.D[p] = c;
-            cnt += c != 0;
-            iu = im;
-            im = id;
+        for (int yb = y0; yb < y1; yb += KB) {
+            Row3 idb[KB];
+            uint32_t bb[KB];
+#pragma unroll
+            for (int j = 0; j < KB; ++j) {
+                if (yb + j < y1) {
+                    idb[j] = row3(g.I, p + (j + 1) * g.S);
+                    bb[j] = g.B[p + j * g.S];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < KB; ++j) {
+                if (yb + j >= y1) break;
+                const Row3 id = idb[j];
+                const uint32_t pre = (t ? im.c : ~im.c) & ~bb[j];
+                uint32_t c = 0;
+                if (pre)
+                    c = pre & simple_bits<FG>(from_west(iu.l, iu.c), iu.c, from_east(iu.c, iu.r),
+                                              from_west(im.l, im.c), from_east(im.c, im.r), from_west(id.l, id.c),
+                                              id.c, from_east(id.c, id.r));
+                g.C[p] = c;
+                g.D[p] = c;
+                cnt += c != 0;
+                iu = im;
+                im = id;
+                p += g.S;
+            }
         }
     };
     walk_strips(g, [&](int x, int y0, int y1, int) { strip(x, y0, y1); });
@@ -1097,9 +1188,47 @@ __device__ __forceinline__ void rebuild_dense(const Img &g, int t, int *counter)
 }
 
 // active-word list from the C plane (needed when a sparse sweep follows a
-// dense one or the E-pass, which only count)
+// dense one or the E-pass, which only count).  Planes outside shared memory
+// (BATCH): the C words of up to 32 rows of a strip are loaded in batches of 8,
+// then ONE warp-aggregated append (a single counter atomic) lists them --
+// a load and an atomic round trip per row otherwise.
+template <bool BATCH>
 __device__ __forceinline__ void build_list(const Img &g, int *counter) {
-    for_strip(g, [&](int y, int x, int p) { append(g.C[p] != 0, (uint32_t)p, g.list, counter); });
+    if constexpr (!BATCH) {
+        for_strip(g, [&](int y, int x, int p) { append(g.C[p] != 0, (uint32_t)p, g.list, counter); });
+    } else {
+        const int lane = threadIdx.x & 31;
+        for (int s0 = g.tid - lane; s0 < g.nstrips; s0 += g.nthr) {   // warp-uniform trip counts
+            const int s = s0 + lane;
+            const bool valid = s < g.nstrips;
+            const int blk = valid ? s / g.WW : 0, x = valid ? s - blk * g.WW : 0;
+            const int y0 = blk * g.hb, y1 = valid ? min(g.H, y0 + g.hb) : y0;
+            for (int yc = 0; yc < g.hb; yc += 32) {
+                const int pb = pidx(g, y0 + yc, x);
+                uint32_t nz = 0;
+                for (int jb = 0; jb < 32 && yc + jb < g.hb; jb += 8) {
+                    uint32_t c[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) c[j] = (y0 + yc + jb + j < y1) ? g.C[pb + (jb + j) * g.S] : 0u;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) nz |= (c[j] != 0u ? 1u : 0u) << (jb + j);
+                }
+                const int cnt = __popc(nz);
+                int incl = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int o = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += o;
+                }
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                if (tot == 0) continue;
+                int base = 0;
+                if (lane == 31) base = atomicAdd(counter, tot);
+                base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+                for (; nz; nz &= nz - 1) g.list[base++] = (uint32_t)(pb + (__ffs(nz) - 1) * g.S);
+            }
+        }
+    }
 }
 
 struct Stats {
@@ -1293,8 +1422,8 @@ struct SweepOut {
 
 // Tiny-sweep regime (single-CTA images): while the list holds <= 32 words,
 // warp 0 runs whole sweeps alone -- fixpoint passes, apply, and re-examination
-// of the 3x3 word neighbourhoods of the flipped words (the words rebuild_sparse
-// would find in the dirty bitmap; the bitmap only deduplicates them here and
+// of the 3x3 word neighbourhoods of the flipped words (the words a scan of the
+// dirty bitmap would find; the bitmap only deduplicates them here and
 // is left zero) -- with warp syncs only, no CTA barrier per sweep.  The new
 // list keeps the engine precondition; the pass counter is not advanced (tiny
 // sweeps use no stamps).  The new list length is left in counters[cur].
@@ -1618,14 +1747,88 @@ __device__ __forceinline__ void claim_pass(const Img &g, const uint32_t *list, i
     }
 }
 
+// ---- global-plane kernels: every phase of a sweep as its own function ------
+// With the planes in L2 the per-thread state of a phase is mostly 64-bit plane
+// pointers; inlined together the phases of a sweep exceeded the register
+// budget (64 registers at 1024 threads) and 15% of the executed instructions
+// of the c2 dense sweeps were local-memory spill traffic (ncu: 5.7 G L2
+// sectors of local traffic against 7.2 G of global).  As separate functions
+// each phase materialises only the pointers it uses.
+#ifndef TS_SPLIT
+#define TS_SPLIT 1
+#endif
+
+template <int FG>
+__device__ __noinline__ int dpass_nl(const View &v, int pc) {
+    const Img g = make_img<false>(v);
+    int evals = 0;
+    if constexpr (kDensePipe)
+        dense_pass_l2<FG>(g, pc, evals);
+    else
+        dense_pass_l2_plain<FG>(g, pc, evals);
+    return evals;
+}
+
+static __device__ __noinline__ void collect_nl(const View &v, int stamp, uint32_t *list, int *counter) {
+    const Img g = make_img<false>(v);
+    collect_stamped(g, (uint8_t)stamp, list, counter);
+}
+
+template <int FG>
+__device__ __noinline__ int claim_pass_nl(const View &v, const uint32_t *list, int n, int jq, uint32_t *next,
+                                          int *ncount) {
+    const Img g = make_img<false>(v);
+    int evals = 0;
+    claim_pass<FG>(g, list, n, g.claim + (jq & 1) * g.mw, g.claim + ((jq + 1) & 1) * g.mw, next, ncount, evals);
+    return evals;
+}
+
+// apply after a dense sweep: the decisions of 8 rows, then the image words of
+// the flipping ones, are requested together
+static __device__ __noinline__ unsigned apply_dense_nl(const View &v) {
+    const Img g = make_img<false>(v);
+    unsigned flips = 0;
+    walk_strips(g, [&](int x, int y0, int y1, int) {
+        constexpr int kB = 8;
+        int p = pidx(g, y0, x);
+        for (int yb = y0; yb < y1; yb += kB, p += kB * g.S) {
+            uint32_t dw[kB], iw[kB];
+#pragma unroll
+            for (int j = 0; j < kB; ++j) dw[j] = yb + j < y1 ? g.D[p + j * g.S] : 0u;
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (dw[j]) iw[j] = g.I[p + j * g.S];
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                if (dw[j]) {
+                    g.I[p + j * g.S] = iw[j] ^ dw[j];
+                    g.D[p + j * g.S] = 0;
+                    flips += __popc(dw[j]);
+                }
+            }
+        }
+    });
+    return flips;
+}
+
+static __device__ __noinline__ unsigned apply_list_nl(const View &v, int n) {
+    const Img g = make_img<false>(v);
+    unsigned flips = 0;
+    for (int sl = g.tid; sl < n; sl += g.nthr) {
+        const int p = (int)g.list[sl];
+        flips += apply_word(g, p, g.D[p]);
+    }
+    return flips;
+}
+
 // Passes j, j+1, ... until one claims nothing.  Pass j reads lists[j & 1]
 // (n words), claims into bitmap j & 1 and list (j + 1) & 1 counted in
 // lcount[(j + 1) % 3], clears bitmap (j + 1) & 1 and zeroes lcount[(j + 2) % 3]
 // (last read before the previous barrier).  Between sweeps both bitmaps are
 // zero and lcount[] is reset by the engine after the post-sweep barrier.
-template <int FG>
-__device__ __forceinline__ void claim_passes(const Img &g, uint32_t *const (&lists)[2], int j, int n, long long cap,
-                                             SweepOut &o) {
+template <int FG, bool SPLIT>
+__device__ __forceinline__ void claim_passes(const View &v, const Img &g, uint32_t *const (&lists)[2], int j, int n,
+                                             long long cap, SweepOut &o) {
     Shared &sh = *g.sh;
     while (n > 0) {
         if (o.passes > cap) {
@@ -1633,8 +1836,11 @@ __device__ __forceinline__ void claim_passes(const Img &g, uint32_t *const (&lis
             break;
         }
         if (g.tid == 0) sh.lcount[(j + 2) % 3] = 0;
-        claim_pass<FG>(g, lists[j & 1], n, g.claim + (j & 1) * g.mw, g.claim + ((j + 1) & 1) * g.mw,
-                       lists[(j + 1) & 1], &sh.lcount[(j + 1) % 3], o.evals);
+        if constexpr (SPLIT)
+            o.evals += claim_pass_nl<FG>(v, lists[j & 1], n, j, lists[(j + 1) & 1], &sh.lcount[(j + 1) % 3]);
+        else
+            claim_pass<FG>(g, lists[j & 1], n, g.claim + (j & 1) * g.mw, g.claim + ((j + 1) & 1) * g.mw,
+                           lists[(j + 1) & 1], &sh.lcount[(j + 1) % 3], o.evals);
         ++o.passes;
         team_sync(g);
         n = *reinterpret_cast<volatile int *>(&sh.lcount[(j + 1) % 3]);
@@ -1644,21 +1850,27 @@ __device__ __forceinline__ void claim_passes(const Img &g, uint32_t *const (&lis
 
 // list sweep (> 32 listed words): a claim pass over the sweep list, then
 // claim passes until none claims; then apply
-template <int FG>
-__device__ __forceinline__ SweepOut list_sweep(const Img &g, int n, long long cap, int pc0) {
+template <int FG, bool SPLIT>
+__device__ __forceinline__ SweepOut list_sweep(const View &v, const Img &g, int n, long long cap) {
     SweepOut o{0, 0, 0, false};
-    (void)pc0;
     Shared &sh = *g.sh;
     uint32_t *const lists[2] = {g.list + g.plen, g.list + g.plen + g.plen / 2};   // each >= nwords / 2 >= n
     if (g.tid == 0) sh.dcount = 0;
     // pass 1 (j = 1): the sweep list; its claims become lists[0] (lcount[2])
-    claim_pass<FG>(g, g.list, n, g.claim + g.mw, g.claim, lists[0], &sh.lcount[2], o.evals);
+    if constexpr (SPLIT)
+        o.evals += claim_pass_nl<FG>(v, g.list, n, 1, lists[0], &sh.lcount[2]);
+    else
+        claim_pass<FG>(g, g.list, n, g.claim + g.mw, g.claim, lists[0], &sh.lcount[2], o.evals);
     ++o.passes;
     team_sync(g);
-    claim_passes<FG>(g, lists, 2, *reinterpret_cast<volatile int *>(&sh.lcount[2]), cap, o);
-    for (int sl = g.tid; sl < n; sl += g.nthr) {
-        const int p = (int)g.list[sl];
-        o.flips += apply_word(g, p, g.D[p]);
+    claim_passes<FG, SPLIT>(v, g, lists, 2, *reinterpret_cast<volatile int *>(&sh.lcount[2]), cap, o);
+    if constexpr (SPLIT) {
+        o.flips += apply_list_nl(v, n);
+    } else {
+        for (int sl = g.tid; sl < n; sl += g.nthr) {
+            const int p = (int)g.list[sl];
+            o.flips += apply_word(g, p, g.D[p]);
+        }
     }
     return o;
 }
@@ -1666,17 +1878,22 @@ __device__ __forceinline__ SweepOut list_sweep(const Img &g, int n, long long ca
 // dense sweep: one strip-walk pass, then compacted passes until no candidate
 // word is stamped; then apply (all threads)
 template <int FG, bool HOT>
-__device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int pc0, bool timing) {
+__device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, long long cap, int pc0, bool timing) {
+    constexpr bool SPLIT = !HOT && TS_SPLIT;
     SweepOut o{0, 0, 0, false};
     int pc = pc0;
     Shared &sh = *g.sh;
     uint32_t *const lists[2] = {g.list, g.list + g.plen};
     const bool tm = timing && g.tid == 0;
     long long t0 = tm ? clock64() : 0;
-    if (HOT)
+    if constexpr (HOT)
         dense_pass<FG>(g, pc, o.evals);
-    else
+    else if constexpr (SPLIT)
+        o.evals += dpass_nl<FG>(v, pc);
+    else if constexpr (kDensePipe)
         dense_pass_l2<FG>(g, pc, o.evals);
+    else
+        dense_pass_l2_plain<FG>(g, pc, o.evals);
     ++o.passes;
     ++pc;
     team_sync(g);   // stamps of the strip-walk pass complete
@@ -1687,7 +1904,10 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
     }
     // the strip walk stamped densely: gather the stamped candidate words by a
     // scan (j = 2's list, lcount[2]); later passes build their lists by claims
-    collect_stamped(g, (uint8_t)pc, lists[0], &sh.lcount[2]);
+    if constexpr (SPLIT)
+        collect_nl(v, pc, lists[0], &sh.lcount[2]);
+    else
+        collect_stamped(g, (uint8_t)pc, lists[0], &sh.lcount[2]);
     team_sync(g);
     const int n2 = *reinterpret_cast<volatile int *>(&sh.lcount[2]);
     if (tm) {
@@ -1696,71 +1916,57 @@ __device__ __forceinline__ SweepOut dense_sweep(const Img &g, long long cap, int
         sh.dtime[3] += n2;
         t0 = t1;
     }
-    claim_passes<FG>(g, lists, 2, n2, cap, o);
+    claim_passes<FG, SPLIT>(v, g, lists, 2, n2, cap, o);
     if (tm) sh.dtime[2] += clock64() - t0;
-    for_strip(g, [&](int y, int x, int p) {
-        const uint32_t dw = g.D[p];
-        if (dw) {
-            g.I[p] ^= dw;
-            g.D[p] = 0;
-            o.flips += __popc(dw);
-        }
-    });
-    return o;
-}
-
-// sparse sweep over the n listed words, then apply (all threads)
-template <int FG>
-__device__ __forceinline__ SweepOut sparse_sweep(const Img &g, int n, long long cap, int pc0) {
-    if (n > 32) return list_sweep<FG>(g, n, cap, pc0);
-    const int tid = g.tid, warp = tid >> 5;
-    SweepOut o{0, 0, 0, false};
-    Slot s0;
-    const bool has0 = tid < n;
-    if (has0) load_slot<FG>(g, g.list[tid], s0);
-    if (n <= 32) {
-        // tiny sweep: one warp iterates to the fixpoint with warp syncs only
-        if (warp == 0) {
-            while (true) {
-                const bool ch = has0 && update_slot<FG, false>(g, s0);
-                ++o.passes;
-                __syncwarp();
-                if (!__any_sync(0xffffffffu, ch)) break;
-                if (o.passes > cap) {
-                    o.bad = true;
-                    break;
-                }
+    if constexpr (SPLIT) {
+        o.flips += apply_dense_nl(v);
+    } else {
+        for_strip(g, [&](int y, int x, int p) {
+            const uint32_t dw = g.D[p];
+            if (dw) {
+                g.I[p] ^= dw;
+                g.D[p] = 0;
+                o.flips += __popc(dw);
             }
-            if (has0) o.flips += apply_word(g, s0.p, s0.d);
-        }
+        });
     }
     return o;
 }
 
 // the sweeps as separate functions: each gets its own register allocation
+// (sweeps of <= 32 words run in the tiny regime, tiny_sweeps)
 template <int FG, bool HOT>
 __device__ __noinline__ SweepOut dense_sweep_nl(const View &v, long long cap, int pc, bool timing) {
     const Img g = make_img<HOT>(v);
-    return dense_sweep<FG, HOT>(g, cap, pc, timing);
+    return dense_sweep<FG, HOT>(v, g, cap, pc, timing);
 }
 
 template <int FG, bool HOT>
 __device__ __noinline__ SweepOut sparse_sweep_nl(const View &v, int n, long long cap, int pc) {
     const Img g = make_img<HOT>(v);
-    return sparse_sweep<FG>(g, n, cap, pc);
+    (void)pc;
+    return list_sweep<FG, !HOT && TS_SPLIT>(v, g, n, cap);
 }
 
-// re-examination after a sweep: all words (dense), the compacted dirty words
-// (list sweeps; the compacted lists' space is free again) or the dirty bitmap
-// by warps (a team's warp-only sweeps)
-template <int FG>
-__device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int n, int t, int *counter) {
+// re-examination after a sweep: all words (dense) or the compacted dirty words
+// (list sweeps; the compacted lists' space is free again)
+template <int FG, bool HOT>
+__device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int t, int *counter) {
     if (dense)
-        rebuild_dense<FG>(g, t, counter);
-    else if (n > 32)
-        rebuild_compact<FG>(g, t, g.list + g.plen, &g.sh->dcount, counter);
+        rebuild_dense<FG, HOT ? 1 : kStreamBatch>(g, t, counter);
     else
-        rebuild_sparse<FG>(g, t, counter);
+        rebuild_compact<FG>(g, t, g.list + g.plen, &g.sh->dcount, counter);
+}
+
+template <int FG>
+__device__ __noinline__ void rebuild_nl(const View &v, bool dense, int t, int *counter) {
+    const Img g = make_img<false>(v);
+    rebuild_any<FG, false>(g, dense, t, counter);
+}
+
+static __device__ __noinline__ void build_list_nl(const View &v, int *counter) {
+    const Img g = make_img<false>(v);
+    build_list<true>(g, counter);
 }
 
 // discard a prepared sweep (max_iter reached): D and C back to zero
@@ -1820,12 +2026,20 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
             sh.ystat[3] += 1;
         }
         const long long cap = 32LL * n + 4;   // DAG depth <= #candidates
-        const bool tiny = g.G == 1 && n <= 32;   // warp-resident regime (needs the list)
+        // warp-resident regime (needs the list).  Teams too: warp 0 of the
+        // team's rank-0 CTA runs the sweeps alone (its own writes are coherent
+        // in its L1, write-through to L2); the team barriers around it publish
+        // the planes in both directions -- 2 team barriers per regime instead
+        // of ~5 per sweep plus a scan of the whole dirty bitmap
+        const bool tiny = n <= 32;
         const bool dense = n > g.dense_min && !tiny;
         if (!dense && !list_ok) {   // sparse sweep after a counting pass: build the list
             if (tid == 0) sh.counters[cur ^ 1] = 0;
             team_sync(g);
-            build_list(g, &sh.counters[cur ^ 1]);
+            if constexpr (!HOT && TS_SPLIT)
+                build_list_nl(v, &sh.counters[cur ^ 1]);
+            else
+                build_list<!HOT>(g, &sh.counters[cur ^ 1]);
             team_sync(g);
             list_ok = true;
             if (st.timing && tid == 0 && n > 512) {
@@ -1837,7 +2051,7 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
         if (tiny) {
             long long budget = sweep_cap - sweeps;
             if (max_sweeps >= 0) budget = min(budget, max_sweeps - sweeps);
-            if (tid < 32) {
+            if (tid < 32) {   // (tid is the team thread id)
                 const TinyOut to = tiny_sweeps<FG, HOT>(v, t, cur, budget, st.timing);
                 if (tid == 0) {
                     sh.bad = to.bad ? 1 : 0;
@@ -1857,11 +2071,11 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
                     }
                 }
             }
-            __syncthreads();
+            team_sync(g);
             sweeps += *reinterpret_cast<volatile long long *>(&sh.tiny[0]);
             st.passes += *reinterpret_cast<volatile long long *>(&sh.tiny[1]);
             const bool tbad = *reinterpret_cast<volatile int *>(&sh.bad) != 0;
-            __syncthreads();   // shared results read before they can be rewritten
+            team_sync(g);   // shared results read before they can be rewritten
             if (st.timing && tid == 0) {
                 sh.xstat[0] += clock64() - tj0;
                 sh.xstat[1] += 1;
@@ -1888,9 +2102,9 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
             if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
             break;
         }
-        // pass counter must stay team-uniform: tiny sweeps (one warp, no stamps)
-        // do not advance it; dense and list sweeps count passes uniformly
-        if (dense || n > 32) pc += (int)o.passes;
+        // pass counter stays team-uniform: dense and list sweeps count passes
+        // uniformly (the tiny regime, one warp and no stamps, does not advance it)
+        pc += (int)o.passes;
         if (st.timing) {
             const int ev = __reduce_add_sync(0xffffffffu, o.evals);
             const unsigned fl = __reduce_add_sync(0xffffffffu, o.flips);
@@ -1901,7 +2115,10 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
         }
         const long long tj1 = st.timing ? clock64() : 0;
         cur ^= 1;
-        rebuild_any<FG>(g, dense, n, t, &sh.counters[cur]);
+        if constexpr (!HOT && TS_SPLIT)
+            rebuild_nl<FG>(v, dense, t, &sh.counters[cur]);
+        else
+            rebuild_any<FG, HOT>(g, dense, t, &sh.counters[cur]);
         list_ok = !dense;
         team_sync(g);
         ++sweeps;

@@ -2,7 +2,15 @@
 #pragma once
 #include <cstdint>
 
+// threads per CTA of the "wide" flavour of the global-plane kernel (cluster
+// teams of large images; ts_hasf_{8,4}g1024.cu).  Measured on c2 (32 x 2048^2,
+// teams of 4): 512 threads (128 registers) 37.2 ms, 768 (80) 35.1 ms, 1024 (64,
+// spill-bound strip walk) 38.3 ms.
+#ifndef TS_WIDE_THREADS
+#define TS_WIDE_THREADS 768
+#endif
 namespace ts {
+constexpr int kWideThreads = TS_WIDE_THREADS;
 
 // Per-image working buffers of the fused HASF kernel.  Each lives either in
 // the CTA's shared memory or in its private slice of a global workspace

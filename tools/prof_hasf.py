@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--dense-div", type=int, default=0)
     ap.add_argument("--team", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--cluster-teams", type=int, default=-1)
     ap.add_argument("--verify", type=int, default=0, help="images checked bit-exact vs the oracle")
     args = ap.parse_args()
     import torch
@@ -41,6 +42,8 @@ def main():
         _lib.load().ts_set_team_size(args.team)
     if args.threads > 0:
         _lib.load().ts_set_cta_threads(args.threads)
+    if args.cluster_teams >= 0:
+        _lib.load().ts_set_cluster_teams(args.cluster_teams)
     args.n = args.n or cfg.n
     imgs_np = W.config_batch(cfg, args.start, args.n)
     imgs = torch.from_numpy(imgs_np).cuda()
