@@ -8,6 +8,9 @@
 #ifdef TS_IMPL_E4_HOT
 #define TS_IMPL_E4 1   // A-B experiment: 4 precedence planes in the 512-thread hot variant too
 #endif
+#ifndef TS_DENSE_PREFETCH
+#define TS_DENSE_PREFETCH 1   // E masks (L2) of the next row requested before the current row is evaluated
+#endif
 #include "ts_hasf_impl.cuh"
 
 namespace ts {

@@ -4,5 +4,5 @@ args="$1"; shift
 for lib in "$@"; do
   if [ "$lib" = cur ]; then unset TS_LIB_PATH; else export TS_LIB_PATH=$PWD/alt/$lib.so; fi
   echo -n "$lib [$args]: "
-  python tools/prof_hasf.py $args --repeat 4 --stats 0 | python -c "import json,sys; d=json.load(sys.stdin); print('%.3f' % d['ms_min'])"
+  python tools/prof_hasf.py $args --repeat 4 --stats 0 | python -c "import json,sys; d=json.load(sys.stdin); print('%.3f' % d['ms_min'], d.get('verify_bad',''))"
 done
