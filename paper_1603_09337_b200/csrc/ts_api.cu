@@ -9,9 +9,11 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <climits>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <string>
@@ -978,6 +980,10 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
         if (ha) good = pack_images(avoid_host + i0 * img, ha + i0 * wimg, cnt, h, w, ww) && good;
         return good;
     };
+    static const bool htrace = getenv("TS_HOST_TRACE") != nullptr;   // debug: host timeline of the call on stderr
+    const auto ht0 = std::chrono::steady_clock::now();
+    auto hnow = [&]() { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ht0).count(); };
+    std::vector<double> tr_send(nchunks, 0.0), tr_back(nchunks, 0.0), tr_unp(nchunks, 0.0);
     // chunk 0 packed (and validated) before anything is enqueued
     if (!pack_chunk(0, std::min<int64_t>(chunk, n)))
         return fail(TS_ERR_VALUE, "binary image pixels must be 0 or 1");   // grid.py:60-61
@@ -1013,6 +1019,7 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
         if (!bad && da && e == cudaSuccess)
             e = cudaMemcpyAsync(da + i0 * wimg, ha + i0 * wimg, cnt * wimg * 4, cudaMemcpyHostToDevice, sin);
         if (e == cudaSuccess) mrc = mo.write(sin, (unsigned long long)(uintptr_t)(ready + k), 1u, kWriteDefault);
+        if (htrace) tr_send[k] = hnow();
     };
     if (e == cudaSuccess) send(0);
     if (e == cudaSuccess && mrc == 0)
@@ -1043,7 +1050,9 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
         for (int k = 0; k < nchunks && e == cudaSuccess && mrc == 0 && !bad; ++k) {
             const int64_t i0 = k * chunk, cnt = std::min<int64_t>(chunk, n - i0);
             e = cudaEventSynchronize(eo[k]);
+            if (htrace) tr_back[k] = hnow();
             if (e == cudaSuccess) unpack_images(hout + i0 * wimg, out_host + i0 * img, cnt, h, w, ww);
+            if (htrace) tr_unp[k] = hnow();
         }
     }
     // the user stream (which frees the buffers) waits for all three streams,
@@ -1064,6 +1073,11 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
     cudaFreeAsync(err, user);
     cudaError_t se = cudaStreamSynchronize(user);
     give_flags(dev, flags);
+    if (htrace) {   // TS_HOST_TRACE: when each chunk was sent, copied back and unpacked (tools/e2e_trace.py)
+        fprintf(stderr, "[ts host trace] n=%lld chunks=%d end=%.0f us\n  k: sent / copied back / unpacked (us)\n", (long long)n,
+                nchunks, hnow());
+        for (int k = 0; k < nchunks; ++k) fprintf(stderr, "  %2d: %6.0f %6.0f %6.0f\n", k, tr_send[k], tr_back[k], tr_unp[k]);
+    }
     if (rc) {
         g_err = keep_msg;
         return rc;
