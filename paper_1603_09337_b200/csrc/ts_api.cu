@@ -159,6 +159,10 @@ std::atomic<int> g_seg_fine{[] {
     const char *e = getenv("TS_SEG_FINE");
     return e ? atoi(e) : 2;
 }()};
+std::atomic<int> g_scan_div{[] {
+    const char *e = getenv("TS_SCAN_DIV");
+    return e ? atoi(e) : -1;
+}()};   // cooperative teams: scan passes (< 0: until the fixpoint, 0: off, d: while > threads / d words change)
 std::atomic<int> g_dense_div{4};   // measured: 4 beats 2 by ~1.5% on c1, neutral on c4
 
 // strip mapping (thread t -> word column t % WW, row block t / WW) and the
@@ -536,6 +540,13 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.pad = pl.pad;
     p.mwords = pl.mwords;
     p.dense_min = pl.dense_min;
+    {   // scan passes (scan_pass) in the dense sweeps of cooperative teams (c3): until the fixpoint by
+        // default; TS_SCAN_DIV = d > 0 stops them once <= team threads / d words change, 0 disables them
+        const int div = g_scan_div.load();
+        p.scan_min = -1;
+        if (!pl.hot && team > 8 && cluster != team && div != 0)
+            p.scan_min = div < 0 ? 0 : (int)std::min<long long>(INT_MAX, (long long)pl.threads * team / div);
+    }
     p.smem_mask = pl.mask;
     p.hot = pl.hot ? 1 : 0;
     for (int b = 0; b < B_COUNT; ++b) p.off[b] = pl.off[b];

@@ -100,6 +100,7 @@ struct Img {
     int nblk, hb;        // strip mapping: row blocks per column, rows per block
     int nstrips;         // nblk * WW strips; thread walks strips tid, tid + nthr, ...
     int dense_min;       // sweeps with more listed words run in dense mode
+    int scan_min;        // teams: scan passes while more words than this change per pass (< 0: none)
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
     int cs;              // thread-block cluster size of the team's launch (1: none; G: the team is one cluster)
@@ -320,6 +321,13 @@ __device__ __forceinline__ void append(bool has, uint32_t entry, uint32_t *list,
     if (lane == leader) base = atomicAdd(counter, __popc(m));
     base = __shfl_sync(act, base, leader);
     if (has) list[base + __popc(m & ((1u << lane) - 1u))] = entry;
+}
+
+// adds per-thread counts to a counter; the warp may have diverged before
+__device__ __forceinline__ void add_count_partial(int cnt, int *counter) {
+    __syncwarp();
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(counter, cnt);
 }
 
 // adds per-thread counts to a shared/global counter (all threads call)
@@ -1285,7 +1293,8 @@ struct Shared {
     int bad;
     unsigned long long flips, evals;
     long long tiny[2];   // tiny-sweep regime results (warp 0 -> CTA): sweeps, passes
-    int lcount[3];       // lengths of the compacted re-evaluation lists (rotating, see claim_passes)
+    int lcount[6];       // [0..2] lengths of the compacted re-evaluation lists (rotating, see claim_passes);
+                         // [3..5] words changed by the scan passes (rotating, see dense_sweep)
     int dcount;          // dirty words listed for re-examination after a list sweep
     long long dtime[4];  // stats: dense pass-1 / collect / list-pass cycles, listed words
     long long sstat[4];  // stats: list sweeps (33..512 words) count / cycles, (> 512) count / cycles
@@ -1311,7 +1320,7 @@ struct View {
     unsigned long long I, D, C, dirty, mark;   // shared address (HOT) or pointer bits
     uint32_t *list, *E, *XS, *R, *K, *A;
     unsigned long long B, claim;   // shared address (HOT) or pointer bits
-    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, fused, mw;
+    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, scan_min, fused, mw;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank, cs;
@@ -1355,6 +1364,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.hb = v.hb;
     g.nstrips = v.nstrips;
     g.dense_min = v.dense_min;
+    g.scan_min = v.scan_min;
     g.lastmask = v.lastmask;
     // HOT implies a single CTA per image: constants, so team code folds away
     g.G = HOT ? 1 : v.G;
@@ -1855,6 +1865,55 @@ static __device__ __noinline__ unsigned apply_list_nl(const View &v, int n) {
     return flips;
 }
 
+// Scan pass (teams, planes in L2): every thread scans 16 stamps, evaluates the
+// candidate words stamped `cur` (word fix) and stamps `next` on the words a
+// change affects -- no list, no claim bitmap, no counter atomics.  A listed
+// evaluation over L2 is a chain of five dependent round trips (list entry,
+// planes, neighbours' candidates, claim atomic, list counter: ~10 K cycles per
+// word and thread on c3); here it is two (stamps, planes), the stamps are
+// fire-and-forget byte stores, and a thread's words are neighbours (L1 hits).
+// Measured on c3 (148-CTA cooperative team): all compacted passes of the dense
+// sweeps as scan passes 19.5 -> 18.3 ms; stopping at a change threshold and
+// finishing with claim passes was in between; two words in flight per thread
+// were slower (20.2 ms).  On c2 (cluster teams of 4: 43 words per thread) the
+// scan itself costs more than the lists save (35.1 -> 36.7 ms), so only the
+// cooperative teams use it (KParams::scan_min).  Returns through *counter the
+// number of words changed (0: fixpoint).
+template <int FG>
+__device__ __forceinline__ void scan_pass(const Img &g, uint8_t cur, uint8_t next, int *counter, int &evals) {
+    const int nchunk = (g.plen + 15) >> 4;   // 16 stamps per uint4
+    const uint32_t vv = 0x01010101u * cur;
+    const int lane = threadIdx.x & 31;
+    int changed = 0;
+    for (int c0 = g.tid - lane; c0 < nchunk; c0 += g.nthr) {
+        const int ch = c0 + lane;
+        if (ch >= nchunk) continue;
+        const uint4 m = reinterpret_cast<const uint4 *>(g.mark)[ch];
+        const uint32_t h = ((__vcmpeq4(m.x, vv) & 0x01010101u) * 0x10204080u) >> 28 |
+                           (((__vcmpeq4(m.y, vv) & 0x01010101u) * 0x10204080u) >> 28) << 4 |
+                           (((__vcmpeq4(m.z, vv) & 0x01010101u) * 0x10204080u) >> 28) << 8 |
+                           (((__vcmpeq4(m.w, vv) & 0x01010101u) * 0x10204080u) >> 28) << 12;
+        for (uint32_t t = h; t; t &= t - 1) {
+            const int p = ch * 16 + __ffs(t) - 1;
+            if (p >= g.plen || g.C[p] == 0u) continue;
+            WordEval a;
+            load_eval(g, p, a);
+            const uint32_t nd = solve_eval<FG>(a);
+            ++evals;
+            if (commit_eval(g, a, nd, next)) ++changed;
+        }
+    }
+    add_count_partial(changed, counter);
+}
+
+template <int FG>
+__device__ __noinline__ int scan_pass_nl(const View &v, int cur, int next, int *counter) {
+    const Img g = make_img<false>(v);
+    int evals = 0;
+    scan_pass<FG>(g, (uint8_t)cur, (uint8_t)next, counter, evals);
+    return evals;
+}
+
 // Passes j, j+1, ... until one claims nothing.  Pass j reads lists[j & 1]
 // (n words), claims into bitmap j & 1 and list (j + 1) & 1 counted in
 // lcount[(j + 1) % 3], clears bitmap (j + 1) & 1 and zeroes lcount[(j + 2) % 3]
@@ -1936,6 +1995,29 @@ __device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, lon
         sh.dtime[0] += t1 - t0;
         t0 = t1;
     }
+    bool fixpoint = false;   // a scan pass changed nothing: no stamps left, skip the compacted passes
+    if constexpr (SPLIT) {
+        // scan passes while many words change (see scan_pass); pass k counts
+        // its changes in lcount[3 + k % 3] and zeroes the counter of pass k + 1
+        // (lcount[0..2], the compacted passes' counters, stay zero meanwhile)
+        if (g.scan_min >= 0) {
+            for (int k = 0;; ++k) {
+                if (o.passes > cap) {
+                    o.bad = true;
+                    break;
+                }
+                if (g.tid == 0) sh.lcount[3 + (k + 1) % 3] = 0;   // last read before the previous barrier
+                o.evals += scan_pass_nl<FG>(v, pc, pc + 1, &sh.lcount[3 + k % 3]);
+                ++o.passes;
+                ++pc;
+                team_sync(g);
+                const int nchg = *reinterpret_cast<volatile int *>(&sh.lcount[3 + k % 3]);
+                if (nchg == 0) fixpoint = true;
+                if (nchg <= g.scan_min) break;   // few changes: the words stamped `pc` -> compacted passes
+            }
+        }
+    }
+    if (!fixpoint) {
     // the strip walk stamped densely: gather the stamped candidate words by a
     // scan (j = 2's list, lcount[2]); later passes build their lists by claims
     if constexpr (SPLIT)
@@ -1952,6 +2034,7 @@ __device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, lon
     }
     claim_passes<FG, SPLIT>(v, g, lists, 2, n2, cap, o);
     if (tm) sh.dtime[2] += clock64() - t0;
+    }
     if constexpr (SPLIT) {
         o.flips += apply_dense_nl(v);
     } else {
@@ -2131,7 +2214,8 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
             sh.counters[cur ^ 1] = 0;
         }
         team_sync(g);
-        if (tid == 0) sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = 0;   // all read before that barrier
+        if (tid == 0)   // all read before that barrier
+            sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = sh.lcount[3] = sh.lcount[4] = sh.lcount[5] = 0;
         if (*reinterpret_cast<volatile int *>(&sh.bad)) {
             if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
             break;
@@ -2443,6 +2527,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     vl.nstrips = p.nstrips;
     vl.fused = p.fused;
     vl.dense_min = p.dense_min;
+    vl.scan_min = p.scan_min;
     vl.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
     vl.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;
     vl.G = G;
@@ -2521,7 +2606,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
         const size_t pix = (size_t)img * p.H * p.W;
         if (lead) {
             sh.counters[0] = 0;
-            sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = 0;
+            sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = sh.lcount[3] = sh.lcount[4] = sh.lcount[5] = 0;
             sh.flips = 0;
             sh.evals = 0;
             sh.dtime[0] = sh.dtime[1] = sh.dtime[2] = sh.dtime[3] = 0;

@@ -108,6 +108,7 @@ struct KParams {
     int nstrips;            // strips = nblk * WW (a thread walks strips tid, tid + nthr, ...)
     int nblk, hb;           // strip mapping: row blocks per word column, rows per block
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
+    int scan_min;           // global planes: scan passes while more words than this change per pass (< 0: off)
     int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
     int threads;            // threads per CTA of the variant (512, or 256 = two CTAs per SM)
     void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1, not a cluster)
