@@ -162,7 +162,7 @@ std::atomic<int> g_seg_fine{[] {
 std::atomic<int> g_scan_div{[] {
     const char *e = getenv("TS_SCAN_DIV");
     return e ? atoi(e) : -1;
-}()};   // cooperative teams: scan passes (< 0: until the fixpoint, 0: off, d: while > threads / d words change)
+}()};   // global planes: scan passes (< 0: until the fixpoint, 0: off, d: while > threads / d words change)
 std::atomic<int> g_dense_div{4};   // measured: 4 beats 2 by ~1.5% on c1, neutral on c4
 
 // strip mapping (thread t -> word column t % WW, row block t / WW) and the
@@ -540,15 +540,21 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     p.pad = pl.pad;
     p.mwords = pl.mwords;
     p.dense_min = pl.dense_min;
-    {   // scan passes (scan_pass) in the dense sweeps of cooperative teams (c3): until the fixpoint by
-        // default; TS_SCAN_DIV = d > 0 stops them once <= team threads / d words change, 0 disables them
+    {   // global planes: the dense sweeps run as scan passes (scan_pass) -- a scan over the candidate
+        // plane, then scans over the stamps until the fixpoint -- and with them a sweep is dense down
+        // to 1/12 of the words holding candidates (c2: divisor 6 -> 29.7, 10 -> 29.4, 32 -> 30.1 ms).
+        // Environment (A/B): TS_SCAN_DIV = 0 disables them, d > 0 hands over to the claim passes once
+        // <= threads / d words change; TS_SCAN_FIRST = 0 keeps the strip walk as the first pass;
+        // TS_SCAN_DENSE_DIV sets the divisor; TS_SCAN_SINGLE = 0 excludes single-CTA launches.
+        static const int sfirst = getenv("TS_SCAN_FIRST") ? atoi(getenv("TS_SCAN_FIRST")) : 1;
+        static const int sdd = getenv("TS_SCAN_DENSE_DIV") ? atoi(getenv("TS_SCAN_DENSE_DIV")) : 12;
+        static const int ssingle = getenv("TS_SCAN_SINGLE") ? atoi(getenv("TS_SCAN_SINGLE")) : 1;
         const int div = g_scan_div.load();
         p.scan_min = -1;
-        if (!pl.hot && team > 8 && cluster != team && div != 0)
+        p.scan_first = sfirst;
+        if (!pl.hot && (team > 1 || ssingle) && div != 0)
             p.scan_min = div < 0 ? 0 : (int)std::min<long long>(INT_MAX, (long long)pl.threads * team / div);
-        // with scan passes a dense sweep costs less than the list machinery down to
-        // fewer candidates (c3: divisor 4 -> 18.3 ms, 16 -> 17.7 ms, 64 -> 18.1 ms)
-        if (p.scan_min >= 0) p.dense_min = pl.nwords / std::max(1, 4 * g_dense_div.load());
+        if (p.scan_min >= 0) p.dense_min = pl.nwords / std::max(1, sdd);
     }
     p.smem_mask = pl.mask;
     p.hot = pl.hot ? 1 : 0;

@@ -101,6 +101,7 @@ struct Img {
     int nstrips;         // nblk * WW strips; thread walks strips tid, tid + nthr, ...
     int dense_min;       // sweeps with more listed words run in dense mode
     int scan_min;        // teams: scan passes while more words than this change per pass (< 0: none)
+    int scan_first;      // the first pass of a dense sweep as a scan over the candidate plane too
     // team of CTAs working on this image (G == 1: this CTA alone)
     int G, tid, nthr;    // CTAs, team thread id, team thread count
     int cs;              // thread-block cluster size of the team's launch (1: none; G: the team is one cluster)
@@ -1320,7 +1321,7 @@ struct View {
     unsigned long long I, D, C, dirty, mark;   // shared address (HOT) or pointer bits
     uint32_t *list, *E, *XS, *R, *K, *A;
     unsigned long long B, claim;   // shared address (HOT) or pointer bits
-    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, scan_min, fused, mw;
+    int H, W, WW, S, plen, org, nblk, hb, nstrips, dense_min, scan_min, scan_first, fused, mw;
     uint32_t lastmask;
     unsigned long long sh;   // Shared block: shared address (G == 1) or global pointer (team)
     int G, rank, cs;
@@ -1365,6 +1366,7 @@ __device__ __forceinline__ Img make_img(const View &v) {
     g.nstrips = v.nstrips;
     g.dense_min = v.dense_min;
     g.scan_min = v.scan_min;
+    g.scan_first = v.scan_first;
     g.lastmask = v.lastmask;
     // HOT implies a single CTA per image: constants, so team code folds away
     g.G = HOT ? 1 : v.G;
@@ -1879,22 +1881,59 @@ static __device__ __noinline__ unsigned apply_list_nl(const View &v, int n) {
 // scan itself costs more than the lists save (35.1 -> 36.7 ms), so only the
 // cooperative teams use it (KParams::scan_min).  Returns through *counter the
 // number of words changed (0: fixpoint).
-template <int FG>
+__shared__ uint16_t g_scan_queue[kWarps][512];   // scan_pass: per-warp queue of stamped words (offsets in the warp's 512)
+
+template <int FG, bool FIRST>
 __device__ __forceinline__ void scan_pass(const Img &g, uint8_t cur, uint8_t next, int *counter, int &evals) {
+    // Stamped words cluster (changes spread locally): a thread evaluating its
+    // own 16 stamps would serialise up to 16 evaluations while its warp idles.
+    // So the warp compacts the stamped words of its 512 stamps into a queue in
+    // shared memory (ballot-free prefix sums, no atomics) and the lanes take
+    // queue entries round-robin.
+    uint16_t(&wq)[kWarps][512] = g_scan_queue;
     const int nchunk = (g.plen + 15) >> 4;   // 16 stamps per uint4
     const uint32_t vv = 0x01010101u * cur;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int changed = 0;
-    for (int c0 = g.tid - lane; c0 < nchunk; c0 += g.nthr) {
+    for (int c0 = g.tid - lane; c0 < nchunk; c0 += g.nthr) {   // warp-uniform trip count
         const int ch = c0 + lane;
-        if (ch >= nchunk) continue;
-        const uint4 m = reinterpret_cast<const uint4 *>(g.mark)[ch];
-        const uint32_t h = ((__vcmpeq4(m.x, vv) & 0x01010101u) * 0x10204080u) >> 28 |
-                           (((__vcmpeq4(m.y, vv) & 0x01010101u) * 0x10204080u) >> 28) << 4 |
-                           (((__vcmpeq4(m.z, vv) & 0x01010101u) * 0x10204080u) >> 28) << 8 |
-                           (((__vcmpeq4(m.w, vv) & 0x01010101u) * 0x10204080u) >> 28) << 12;
-        for (uint32_t t = h; t; t &= t - 1) {
-            const int p = ch * 16 + __ffs(t) - 1;
+        uint32_t h = 0;
+        if (ch < nchunk) {
+            if constexpr (FIRST) {
+                // a sweep's first pass: every word holding candidates (instead of
+                // the strip walk, whose warps pay an evaluation for every row in
+                // which any lane has candidates)
+                const uint4 *cp = reinterpret_cast<const uint4 *>(g.C) + (size_t)ch * 4;
+                uint4 c4[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) c4[j] = (ch * 16 + j * 4 < g.plen) ? cp[j] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    h |= ((c4[j].x != 0u ? 1u : 0u) | (c4[j].y != 0u ? 2u : 0u) | (c4[j].z != 0u ? 4u : 0u) |
+                          (c4[j].w != 0u ? 8u : 0u))
+                         << (4 * j);
+            } else {
+                const uint4 m = reinterpret_cast<const uint4 *>(g.mark)[ch];
+                h = ((__vcmpeq4(m.x, vv) & 0x01010101u) * 0x10204080u) >> 28 |
+                    (((__vcmpeq4(m.y, vv) & 0x01010101u) * 0x10204080u) >> 28) << 4 |
+                    (((__vcmpeq4(m.z, vv) & 0x01010101u) * 0x10204080u) >> 28) << 8 |
+                    (((__vcmpeq4(m.w, vv) & 0x01010101u) * 0x10204080u) >> 28) << 12;
+            }
+        }
+        const int cnt = __popc(h);
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot == 0) continue;
+        int at = incl - cnt;
+        for (uint32_t t = h; t; t &= t - 1) wq[warp][at++] = (uint16_t)(lane * 16 + __ffs(t) - 1);
+        __syncwarp();
+        for (int i = lane; i < tot; i += 32) {
+            const int p = c0 * 16 + (int)wq[warp][i];
             if (p >= g.plen || g.C[p] == 0u) continue;
             WordEval a;
             load_eval(g, p, a);
@@ -1902,15 +1941,16 @@ __device__ __forceinline__ void scan_pass(const Img &g, uint8_t cur, uint8_t nex
             ++evals;
             if (commit_eval(g, a, nd, next)) ++changed;
         }
+        __syncwarp();
     }
     add_count_partial(changed, counter);
 }
 
-template <int FG>
+template <int FG, bool FIRST>
 __device__ __noinline__ int scan_pass_nl(const View &v, int cur, int next, int *counter) {
     const Img g = make_img<false>(v);
     int evals = 0;
-    scan_pass<FG>(g, (uint8_t)cur, (uint8_t)next, counter, evals);
+    scan_pass<FG, FIRST>(g, (uint8_t)cur, (uint8_t)next, counter, evals);
     return evals;
 }
 
@@ -1981,8 +2021,12 @@ __device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, lon
     long long t0 = tm ? clock64() : 0;
     if constexpr (HOT)
         dense_pass<FG>(g, pc, o.evals);
-    else if constexpr (SPLIT)
-        o.evals += dpass_nl<FG>(v, pc);
+    else if constexpr (SPLIT) {
+        if (g.scan_min >= 0 && g.scan_first)   // (its change count is not needed: the scan passes follow)
+            o.evals += scan_pass_nl<FG, true>(v, pc, pc + 1, &sh.dcount);
+        else
+            o.evals += dpass_nl<FG>(v, pc);
+    }
     else if constexpr (kDensePipe)
         dense_pass_l2<FG>(g, pc, o.evals);
     else
@@ -2007,7 +2051,7 @@ __device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, lon
                     break;
                 }
                 if (g.tid == 0) sh.lcount[3 + (k + 1) % 3] = 0;   // last read before the previous barrier
-                o.evals += scan_pass_nl<FG>(v, pc, pc + 1, &sh.lcount[3 + k % 3]);
+                o.evals += scan_pass_nl<FG, false>(v, pc, pc + 1, &sh.lcount[3 + k % 3]);
                 ++o.passes;
                 ++pc;
                 team_sync(g);
@@ -2528,6 +2572,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     vl.fused = p.fused;
     vl.dense_min = p.dense_min;
     vl.scan_min = p.scan_min;
+    vl.scan_first = p.scan_first;
     vl.lastmask = (p.W & 31) ? ((1u << (p.W & 31)) - 1u) : ~0u;
     vl.sh = G == 1 ? (unsigned long long)__cvta_generic_to_shared(&sh_local) : (unsigned long long)shp;
     vl.G = G;

@@ -109,6 +109,7 @@ struct KParams {
     int nblk, hb;           // strip mapping: row blocks per word column, rows per block
     int dense_min;          // sweeps with more listed words run in dense (strip) mode
     int scan_min;           // global planes: scan passes while more words than this change per pass (< 0: off)
+    int scan_first;         // dense sweeps start with a scan over the candidate plane instead of the strip walk
     int team;               // CTAs per image (1, or > 1 for the generic variant; cooperative launch)
     int threads;            // threads per CTA of the variant (512, or 256 = two CTAs per SM)
     void *tctl;             // team control blocks, kTeamCtlBytes each, zeroed (team > 1, not a cluster)
