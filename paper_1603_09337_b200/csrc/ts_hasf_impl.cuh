@@ -177,6 +177,37 @@ __device__ __forceinline__ void team_sync(const Img &g) {
         __syncthreads();
 }
 
+// team barrier + the value of a team counter as of the barrier.  Cooperative
+// teams: read by the CTA's polling thread right after its acquire and handed
+// to the CTA through shared memory -- 148 loads of the word instead of one per
+// warp of the chip (2 368), which alone cost ~1 000 cycles per barrier
+// (tools/probe/team_barrier.cu: 2 518 -> 3 577 cycles with the read).
+__device__ __forceinline__ int team_sync_get(const Img &g, const int *ctr) {
+    if (g.G == 1 || g.cs > 1) {   // one CTA, or clusters (the counter is a DSMEM / cluster-local read)
+        team_sync(g);
+        return *reinterpret_cast<const volatile int *>(ctr);
+    }
+    __shared__ int s_val;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned target = (*g.epoch += 1u) * (unsigned)g.G;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.bar) : "memory");
+        long long spins = 0;
+        while (true) {
+            unsigned c;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(g.bar) : "memory");
+            if ((int)(c - target) >= 0) break;
+            if (++spins > (1LL << 27)) {   // ~ seconds
+                set_err(g.err, ERR_TEAM_TIMEOUT);
+                break;
+            }
+        }
+        s_val = *reinterpret_cast<const volatile int *>(ctr);
+    }
+    __syncthreads();
+    return s_val;
+}
+
 struct Nb {
     uint32_t nw, n, ne, w, e, sw, s, se;
     uint32_t m;   // the centre word itself
@@ -1147,7 +1178,7 @@ __device__ __forceinline__ unsigned apply_word(const Img &g, int p, uint32_t dw)
 // re-examination after a list sweep: the dirty bitmap is compacted into a
 // word list (thread per bitmap word, warp prefix sums), then every listed word
 // is re-examined by one thread -- full lanes instead of a warp per bitmap word
-template <int FG>
+template <int FG, bool GET = false>
 __device__ __forceinline__ void rebuild_compact(const Img &g, int t, uint32_t *dl, int *dcount, int *counter) {
     const int lane = threadIdx.x & 31;
     const int nq = (g.plen + 31) >> 5;
@@ -1172,8 +1203,13 @@ __device__ __forceinline__ void rebuild_compact(const Img &g, int t, uint32_t *d
         base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
         for (; bits; bits &= bits - 1) dl[base++] = (uint32_t)(q * 32 + __ffs(bits) - 1);
     }
-    team_sync(g);
-    const int nd = *reinterpret_cast<volatile int *>(dcount);
+    int nd;
+    if constexpr (GET) {
+        nd = team_sync_get(g, dcount);
+    } else {
+        team_sync(g);
+        nd = *reinterpret_cast<volatile int *>(dcount);
+    }
     for (int s0 = g.tid - lane; s0 < nd; s0 += g.nthr) {   // warp-uniform trip count
         const int sl = s0 + lane;
         uint32_t c = 0;
@@ -1975,8 +2011,12 @@ __device__ __forceinline__ void claim_passes(const View &v, const Img &g, uint32
             claim_pass<FG>(g, lists[j & 1], n, g.claim + (j & 1) * g.mw, g.claim + ((j + 1) & 1) * g.mw,
                            lists[(j + 1) & 1], &sh.lcount[(j + 1) % 3], o.evals);
         ++o.passes;
-        team_sync(g);
-        n = *reinterpret_cast<volatile int *>(&sh.lcount[(j + 1) % 3]);
+        if constexpr (SPLIT) {
+            n = team_sync_get(g, &sh.lcount[(j + 1) % 3]);
+        } else {
+            team_sync(g);
+            n = *reinterpret_cast<volatile int *>(&sh.lcount[(j + 1) % 3]);
+        }
         ++j;
     }
 }
@@ -2054,8 +2094,7 @@ __device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, lon
                 o.evals += scan_pass_nl<FG, false>(v, pc, pc + 1, &sh.lcount[3 + k % 3]);
                 ++o.passes;
                 ++pc;
-                team_sync(g);
-                const int nchg = *reinterpret_cast<volatile int *>(&sh.lcount[3 + k % 3]);
+                const int nchg = team_sync_get(g, &sh.lcount[3 + k % 3]);
                 if (nchg == 0) fixpoint = true;
                 if (nchg <= g.scan_min) break;   // few changes: the words stamped `pc` -> compacted passes
             }
@@ -2068,8 +2107,13 @@ __device__ __forceinline__ SweepOut dense_sweep(const View &v, const Img &g, lon
         collect_nl(v, pc, lists[0], &sh.lcount[2]);
     else
         collect_stamped(g, (uint8_t)pc, lists[0], &sh.lcount[2]);
-    team_sync(g);
-    const int n2 = *reinterpret_cast<volatile int *>(&sh.lcount[2]);
+    int n2;
+    if constexpr (SPLIT) {
+        n2 = team_sync_get(g, &sh.lcount[2]);
+    } else {
+        team_sync(g);
+        n2 = *reinterpret_cast<volatile int *>(&sh.lcount[2]);
+    }
     if (tm) {
         const long long t1 = clock64();
         sh.dtime[1] += t1 - t0;
@@ -2116,7 +2160,7 @@ __device__ __forceinline__ void rebuild_any(const Img &g, bool dense, int t, int
     if (dense)
         rebuild_dense<FG, HOT ? 1 : kStreamBatch>(g, t, counter);
     else
-        rebuild_compact<FG>(g, t, g.list + g.plen, &g.sh->dcount, counter);
+        rebuild_compact<FG, !HOT>(g, t, g.list + g.plen, &g.sh->dcount, counter);
 }
 
 template <int FG>
@@ -2170,8 +2214,9 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
     long long sweeps = 0;
     const long long sweep_cap = (long long)g.H * g.W + 2;   // >= 1 flip per sweep, <= 1 flip per pixel
     bool list_ok = false;   // the E-pass and dense re-examination only count candidates
+    int n_next = vcount[cur];   // global planes: handed over by the barrier that ends a sweep
     while (true) {
-        const int n = vcount[cur];
+        const int n = HOT ? vcount[cur] : n_next;
         if (n == 0) break;
         if ((max_sweeps >= 0 && sweeps >= max_sweeps) || sweeps >= sweep_cap) {
             if (sweeps >= sweep_cap && (max_sweeps < 0 || sweeps < max_sweeps)) {
@@ -2246,6 +2291,7 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
                 break;
             }
             if (st.timing) tyl = clock64();
+            if constexpr (!HOT) n_next = vcount[cur];   // left by the tiny regime
             continue;
         }
         SweepOut o;
@@ -2257,10 +2303,16 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
             sh.bad = o.bad ? 1 : 0;
             sh.counters[cur ^ 1] = 0;
         }
-        team_sync(g);
+        int sweep_bad;
+        if constexpr (HOT) {
+            team_sync(g);
+            sweep_bad = 0;
+        } else {
+            sweep_bad = team_sync_get(g, &sh.bad);
+        }
         if (tid == 0)   // all read before that barrier
             sh.lcount[0] = sh.lcount[1] = sh.lcount[2] = sh.lcount[3] = sh.lcount[4] = sh.lcount[5] = 0;
-        if (*reinterpret_cast<volatile int *>(&sh.bad)) {
+        if (HOT ? *reinterpret_cast<volatile int *>(&sh.bad) : sweep_bad) {
             if (tid == 0) set_err(g.err, ERR_JACOBI_CAP);
             break;
         }
@@ -2282,7 +2334,10 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
         else
             rebuild_any<FG, HOT>(g, dense, t, &sh.counters[cur]);
         list_ok = !dense;
-        team_sync(g);
+        if constexpr (HOT)
+            team_sync(g);
+        else
+            n_next = team_sync_get(g, &sh.counters[cur]);
         ++sweeps;
         st.passes += o.passes;
         if (st.timing) {
