@@ -123,6 +123,25 @@ __device__ __forceinline__ void *dsmem_map(void *p, unsigned rank) {
     return r;
 }
 
+#ifdef TS_BAR_TRACE
+// debug build (tools/bar_trace.py): %globaltimer at arrival and release of every
+// cooperative team barrier, per CTA, into the ts_set_trace buffer
+// [barrier][rank][2]
+__shared__ long long *g_bt;
+__shared__ long long g_bt_cap;
+__device__ __forceinline__ void bt_rec(const Img &g, unsigned epoch1, int k) {
+    const long long idx = (long long)(epoch1 - 1u);
+    if (g_bt && idx < g_bt_cap) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_bt[(idx * g.G + g.tid / kThreads) * 2 + k] = (long long)t;
+    }
+}
+#define TS_BT(e, k) bt_rec(g, (e), (k))
+#else
+#define TS_BT(e, k)
+#endif
+
 // Barrier over the G CTAs of a team (co-resident: cooperative launch).  One
 // monotonic arrival counter per team: barrier number k (counted per CTA in
 // *g.epoch; every CTA of a team executes the same barriers) completes when the
@@ -158,6 +177,7 @@ __device__ __forceinline__ void team_sync(const Img &g) {
     if (threadIdx.x == 0) {
         const unsigned target = (*g.epoch += 1u) * parts;   // every CTA counts, leaders arrive
         if (leader) {
+            TS_BT(*g.epoch, 0);
             asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.bar) : "memory");
             long long spins = 0;
             while (true) {
@@ -169,6 +189,7 @@ __device__ __forceinline__ void team_sync(const Img &g) {
                     break;
                 }
             }
+            TS_BT(*g.epoch, 1);
         }
     }
     if (hier)
@@ -191,6 +212,7 @@ __device__ __forceinline__ int team_sync_get(const Img &g, const int *ctr) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned target = (*g.epoch += 1u) * (unsigned)g.G;
+        TS_BT(*g.epoch, 0);
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.bar) : "memory");
         long long spins = 0;
         while (true) {
@@ -203,6 +225,7 @@ __device__ __forceinline__ int team_sync_get(const Img &g, const int *ctr) {
             }
         }
         s_val = *reinterpret_cast<const volatile int *>(ctr);
+        TS_BT(*g.epoch, 1);
     }
     __syncthreads();
     return s_val;
@@ -2353,7 +2376,10 @@ __device__ TS_ENGINE_INLINE int2 engine_nl(const View &v, int t, long long max_s
                 st.n_tiny += 1;
                 st.pass_tiny += o.passes;
             } else if (tid == 0) {
-                const int b = n <= 512 ? 0 : 2;
+#ifndef TS_SSTAT_SPLIT
+#define TS_SSTAT_SPLIT 512   // stats: boundary between the two list-sweep buckets
+#endif
+                const int b = n <= TS_SSTAT_SPLIT ? 0 : 2;
                 sh.sstat[b] += 1;
                 sh.sstat[b + 1] += tj2 - tj0;
                 if (n > 512) {
@@ -2642,6 +2668,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
     if (threadIdx.x == 0) {
         v_shared = vl;
         epoch_local = 0;
+#ifdef TS_BAR_TRACE
+        g_bt = (!HOT && G > 1 && p.cluster <= 1) ? p.trace : nullptr;
+        g_bt_cap = p.trace_cap;
+        if (g_bt) {   // one extra row: the SM each rank runs on
+            unsigned long long smid;
+            asm volatile("{ .reg .u32 s; mov.u32 s, %%smid; cvt.u64.u32 %0, s; }" : "=l"(smid));
+            g_bt[(g_bt_cap * G + rank) * 2] = (long long)smid;
+        }
+#endif
     }
     __syncthreads();
     if (one_cluster) {   // rank 0's control block: zeroed, and every CTA of the cluster running
@@ -2717,7 +2752,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) hasf_kernel(const KParam
             sh.eio = EngineIO{};
         }
         // debug trace: [smid, grabbed, ready, loaded, stages done, stored, end] (%globaltimer ns)
+#ifdef TS_BAR_TRACE
+        const bool tracing = false;   // the buffer holds the barrier trace
+#else
         const bool tracing = p.trace && lead && task < p.trace_cap;
+#endif
         auto stamp = [&](int k) {
             if (!tracing) return;
             unsigned long long t;
