@@ -384,8 +384,10 @@ def main():
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+    # a rendezvous is set up (torchrun, any N): the barriers and the max-over-ranks reduce go through NCCL
+    grouped = world > 1 or ("RANK" in os.environ and "MASTER_ADDR" in os.environ)
+    if grouped:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     if args.smem_budget >= 0:
         _lib.load().ts_set_smem_budget(args.smem_budget)
     _lib.load().ts_set_cluster_teams(args.cluster_teams)
@@ -415,14 +417,14 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if grouped:
         dist.barrier()
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        if world > 1:
+        if grouped:
             dist.barrier()
         clk.mark(True)
         for i in range(args.steps):
@@ -432,7 +434,7 @@ def main():
             ends[i].record(stream)
         torch.cuda.synchronize()
         clk.mark(False)
-        if world > 1:
+        if grouped:
             dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = max_over_ranks(float(sum(step_ms)))
@@ -477,7 +479,7 @@ def main():
 
     e2e_step()
     torch.cuda.synchronize()
-    if world > 1:
+    if grouped:
         dist.barrier()
     t0 = time.perf_counter()
     e_start = torch.cuda.Event(enable_timing=True)
@@ -557,7 +559,7 @@ def main():
             "repo_libs_mapped": repo_libs_mapped(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if grouped:
         dist.destroy_process_group()
     return 0
 

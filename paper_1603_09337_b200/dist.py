@@ -75,11 +75,12 @@ def hasf_sharded(images, r_max: int, adj=None, group=None, fn=None) -> np.ndarra
         from .smoothing import hasf_batch
         fn = hasf_batch
     s0, s1 = shard_range(n, rank, world)
-    dev = "cuda" if world > 1 and dist.get_backend(group) == "nccl" else "cpu"
+    grouped = dist.is_initialized()   # a process group exists (also a single-rank one): gather through it
+    dev = "cuda" if grouped and dist.get_backend(group) == "nccl" else "cpu"
     shard = images[s0:s1]
     mine = fn(torch.from_numpy(shard).to(dev) if dev == "cuda" else shard, r_max, adj)
     mine = mine if isinstance(mine, torch.Tensor) else torch.from_numpy(np.asarray(mine, dtype=np.uint8))
-    if world == 1:
+    if not grouped:
         return mine.cpu().numpy()
     chunk = -(-n // world)   # ceil: equal-size padded chunks for all_gather
     buf = torch.zeros((chunk, h, (w + 7) // 8), dtype=torch.uint8, device=dev)

@@ -635,3 +635,38 @@ def test_nonblocking_batch_and_library_hygiene():
         thr = ctypes.c_uint64()
         assert cudart.cudaMemPoolGetAttribute(pool_h, 4, ctypes.byref(thr)) == 0   # ReleaseThreshold
         assert thr.value == 0
+
+
+def _nccl_worker(port, q):
+    import torch.distributed as dist
+    from paper_1603_09337_b200.dist import hasf_sharded, max_over_ranks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    rng = np.random.default_rng(11)
+    imgs = np.stack([random_image(rng, 40, 75, 0.5) for _ in range(5)])
+    out = hasf_sharded(imgs, 3)                 # device path + bit-packed NCCL all-gather
+    t = max_over_ranks(12.5)                    # device all-reduce (the bench's timing reduce)
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((imgs, out, t))
+
+
+def test_nccl_single_rank_sharded_gather():
+    """The NCCL data path of dist.hasf_sharded / max_over_ranks on the device
+    (one rank: this box has one GPU; world size 2 is covered with gloo on CPU)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_worker, args=(port, q))
+    pr.start()
+    imgs, out, t = q.get(timeout=300)
+    pr.join(timeout=60)
+    assert pr.exitcode == 0
+    assert np.array_equal(out, O.hasf_batch(imgs, 3, 8))
+    assert t == 12.5
