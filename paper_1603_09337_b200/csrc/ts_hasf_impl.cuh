@@ -1663,19 +1663,32 @@ __device__ __forceinline__ void collect_stamped(const Img &g, uint8_t v, uint32_
     const int lane = threadIdx.x & 31;
     for (int c0 = g.tid - lane; c0 < nchunk; c0 += g.nthr) {   // warp-uniform trip count
         const int ch = c0 + lane;
-        uint32_t valid = 0;
+        uint32_t h = 0;
         if (ch < nchunk) {
             const uint4 m = reinterpret_cast<const uint4 *>(g.mark)[ch];
             // one bit per matching stamp byte: byte b of word k -> bit 4k + b
-            const uint32_t h = ((__vcmpeq4(m.x, vv) & 0x01010101u) * 0x10204080u) >> 28 |
-                               (((__vcmpeq4(m.y, vv) & 0x01010101u) * 0x10204080u) >> 28) << 4 |
-                               (((__vcmpeq4(m.z, vv) & 0x01010101u) * 0x10204080u) >> 28) << 8 |
-                               (((__vcmpeq4(m.w, vv) & 0x01010101u) * 0x10204080u) >> 28) << 12;
-            for (uint32_t t = h; t; t &= t - 1) {
-                const int b = __ffs(t) - 1;
-                if (ch * 16 + b < g.plen && g.C[ch * 16 + b]) valid |= 1u << b;
-            }
+            h = ((__vcmpeq4(m.x, vv) & 0x01010101u) * 0x10204080u) >> 28 |
+                (((__vcmpeq4(m.y, vv) & 0x01010101u) * 0x10204080u) >> 28) << 4 |
+                (((__vcmpeq4(m.z, vv) & 0x01010101u) * 0x10204080u) >> 28) << 8 |
+                (((__vcmpeq4(m.w, vv) & 0x01010101u) * 0x10204080u) >> 28) << 12;
         }
+        if (!__any_sync(0xffffffffu, h != 0u)) continue;
+        // which of the warp's 512 words hold candidates: a lane checking its own
+        // 16 consecutive words reads at a 16-word stride (16-way bank conflicts
+        // in shared memory, and a dependent load per stamp: a third of c1's
+        // excess wavefronts); instead the warp reads the 512 words row-wise
+        // (lane l: words 32 j + l, conflict-free, independent) and 16 ballots
+        // hand every lane the bits of its own 16 words
+        uint32_t mine = 0;   // lane j keeps ballot j (words 32 j .. 32 j + 31)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int q = c0 * 16 + j * 32 + lane;
+            const uint32_t cw = q < g.plen ? g.C[q] : 0u;
+            const uint32_t bm = __ballot_sync(0xffffffffu, cw != 0u);
+            if (lane == j) mine = bm;
+        }
+        const uint32_t sel = __shfl_sync(0xffffffffu, mine, lane >> 1);   // words 16 lane .. 16 lane + 15
+        const uint32_t valid = h & ((sel >> (16 * (lane & 1))) & 0xFFFFu);
         const int cnt = __popc(valid);
         int incl = cnt;
 #pragma unroll
