@@ -80,6 +80,24 @@ def main():
     print("  mean lateness vs the barrier's mean arrival (us), worst ranks: " +
           "  ".join(f"{r}:{int(smid[r])}:{late[r]:.2f}" for r in order))
     print(f"  lateness by rank: std {late.std():.2f} us, min {late.min():.2f}, max {late.max():.2f}")
+    # the barriers the team's first CTA arrives last at: by how much, and after how much work
+    r0 = np.nonzero(who == 0)[0]
+    r0 = r0[r0 > 0]
+    if len(r0):
+        second = np.sort(arr[r0], axis=1)[:, -2]
+        gap = arr[r0, 0] - second
+        w0 = work[r0 - 1, 0]
+        wm = np.median(work[r0 - 1], axis=1)
+        print(f"  rank 0 last at {len(r0)} barriers: ahead of it the next CTA by median {np.median(gap):.2f} us "
+              f"(sum {gap.sum():.0f} us); its work before them median {np.median(w0):.2f} us vs the team's median "
+              f"{np.median(wm):.2f} us")
+        edges2 = [0, 2, 5, 10, 20, 50, 1e9]
+        print("    by the team's median work in the interval (us): count, sum of rank 0's gap")
+        for lo, hi in zip(edges2[:-1], edges2[1:]):
+            m = (wm >= lo) & (wm < hi)
+            print(f"      [{lo:>4g}, {hi:>4g}): {int(m.sum()):5d}  {gap[m].sum():8.0f}")
+        d = np.diff(r0)
+        print(f"    spacing of those barriers: median {np.median(d):.0f}, runs of consecutive ones {(d == 1).sum()}")
 
 
 if __name__ == "__main__":
