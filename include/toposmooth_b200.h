@@ -216,8 +216,11 @@ int32_t ts_set_fused_prep(int32_t on);
 int32_t ts_set_segment_stages(int32_t stages);
 
 /* Tuning / A-B: the last `stages` stages of an image run as one-stage
- * segments (the queue's drain then waits for at most one short stage);
- * default 2 (env TS_SEG_FINE).  Returns the previous value. */
+ * segments (the queue's drain then waits for at most one short stage).
+ * Unless this is called (or env TS_SEG_FINE is set, or TS_SEG_TUNE=0), the
+ * blocking device entry picks 2 or 1 per problem (shape, batch, radii,
+ * adjacency, constraints) by timing its own first three launches of it;
+ * the outputs do not depend on the segmentation.  Returns the previous value. */
 int32_t ts_set_segment_fine(int32_t stages);
 
 /* Tuning / A-B: the segmentation used by the streamed host entry

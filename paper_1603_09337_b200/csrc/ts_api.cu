@@ -16,7 +16,9 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/toposmooth_b200.h"
@@ -159,6 +161,29 @@ std::atomic<int> g_seg_fine{[] {
     const char *e = getenv("TS_SEG_FINE");
     return e ? atoi(e) : 2;
 }()};
+// The fine tail is tuned per problem unless the caller fixed it (TS_SEG_FINE,
+// ts_set_segment_fine, TS_SEG_TUNE=0).  Which tail wins depends on how the
+// batch's (segment, image) tasks tile the resident CTAs -- c1 (256 x 512^2 on
+// 148 CTAs) runs 1.7% faster with a tail of 1 than of 2, c4 (1024 x 256^2 on
+// 296) 3.5% slower -- and no closed form predicted it over the measured
+// settings.  The blocking device entry therefore times its own first three
+// launches of a problem (tail 2, tail 1, tail 2: the first launch of a process
+// also pays one-time costs) and keeps the faster tail for that problem; results
+// are identical under every segmentation (tests force every boundary).
+std::atomic<int> g_seg_fine_fixed{[] {
+    const char *t = getenv("TS_SEG_TUNE");
+    return (getenv("TS_SEG_FINE") != nullptr || (t && atoi(t) == 0)) ? 1 : 0;
+}()};
+thread_local int tl_seg_fine = -1;   // >= 0: the fine tail of this thread's next fused launches
+using TuneKey = std::tuple<int, int, long long, int, int, int, int, int, int, int>;
+struct TuneState {
+    int trials = 0;
+    float best[2] = {1e30f, 1e30f};   // candidate 0: tail 2, candidate 1: tail 1
+    int choice = -1;
+};
+constexpr int kTuneFine[2] = {2, 1};
+std::mutex g_tune_mu;
+std::map<TuneKey, TuneState> g_tune;
 std::atomic<int> g_scan_div{[] {
     const char *e = getenv("TS_SCAN_DIV");
     return e ? atoi(e) : -1;
@@ -489,7 +514,7 @@ int fused_launch(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h
     // (the streamed host entry prefers coarser segments: its copy-back and host
     // unpacking overlap the kernel only while images keep completing)
     const int seg_stages = ready ? g_seg_stages_host.load() : g_seg_stages.load();
-    const int fine = std::max(0, ready ? g_seg_fine_host.load() : g_seg_fine.load());
+    const int fine = std::max(0, ready ? g_seg_fine_host.load() : (tl_seg_fine >= 0 ? tl_seg_fine : g_seg_fine.load()));
     int nseg = 1;
     if (mode == MODE_HASF && team == 1 && seg_stages > 0 && (n > pl.per_wave || g_seg_force.load()) &&
         total_stages > 1)
@@ -605,13 +630,49 @@ int run_fused(int mode, const uint8_t *in, uint8_t *out, int64_t n, int32_t h, i
     int *err = nullptr;
     TS_CUDA(ws_malloc((void **)&err, sizeof(int), st));
     cudaError_t me = cudaMemsetAsync(err, 0, sizeof(int), st);
+    // fine-tail tuning (see g_seg_fine_fixed): this call is a trial, or uses the problem's choice
+    const bool tunable = mode == MODE_HASF && !stats_host && !g_seg_fine_fixed.load();
+    const TuneKey key{h, w, (long long)n, r_first, r_last, do_cut, do_fill, fg, keep ? 1 : 0, avoid ? 1 : 0};
+    int trial = -1;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    tl_seg_fine = -1;
+    if (tunable) {
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        auto it = g_tune.find(key);
+        if (it == g_tune.end() && g_tune.size() < 256) it = g_tune.emplace(key, TuneState{}).first;
+        if (it != g_tune.end()) {
+            TuneState &ts = it->second;
+            if (ts.choice >= 0) {
+                tl_seg_fine = kTuneFine[ts.choice];
+            } else if (cudaEventCreate(&t0) == cudaSuccess && cudaEventCreate(&t1) == cudaSuccess) {
+                trial = ts.trials & 1;   // 0, 1, 0
+                tl_seg_fine = kTuneFine[trial];
+            }
+        }
+    }
+    if (trial >= 0) cudaEventRecord(t0, st);
     int rc = me == cudaSuccess ? fused_launch(mode, in, out, n, h, w, r_first, r_last, do_cut, do_fill, fg, keep,
                                               avoid, prio, max_sweeps, st, stats_host, err, nullptr)
                                : cuda_fail(me, "cudaMemsetAsync");
+    if (trial >= 0) cudaEventRecord(t1, st);
+    tl_seg_fine = -1;
     int herr = 0;
     cudaError_t ce = cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaFreeAsync(err, st);
     cudaError_t se = cudaStreamSynchronize(st);
+    if (trial >= 0) {
+        float ms = 0.f;
+        const bool timed = rc == TS_OK && se == cudaSuccess && cudaEventElapsedTime(&ms, t0, t1) == cudaSuccess;
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        auto it = g_tune.find(key);
+        if (it != g_tune.end() && it->second.choice < 0) {
+            TuneState &ts = it->second;
+            if (timed) ts.best[trial] = std::min(ts.best[trial], ms);
+            if (++ts.trials >= 3) ts.choice = ts.best[1] < ts.best[0] ? 1 : 0;
+        }
+    }
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
     if (rc) return rc;
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpyAsync(error flag)");
     if (se != cudaSuccess) return cuda_fail(se, "hasf_kernel");
@@ -762,8 +823,16 @@ int ts_hasf_batch_async(const uint8_t *in_dev, uint8_t *out_dev, int64_t n, int3
     if (r_max > kMaxR) return fail(TS_ERR_UNSUPPORTED, "the non-blocking entry runs radii <= 16 (fused kernel)");
     cudaStream_t st = (cudaStream_t)stream;
     TS_CUDA(cudaMemsetAsync(err_dev, 0, sizeof(int32_t), st));
-    return fused_launch(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr, -1, st,
-                        nullptr, reinterpret_cast<int *>(err_dev), nullptr) ?: ok();
+    tl_seg_fine = -1;   // the fine tail the blocking entry tuned for this problem, if it has
+    if (!g_seg_fine_fixed.load()) {
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        auto it = g_tune.find(TuneKey{h, w, (long long)n, 1, r_max, 1, 1, fg, keep_dev ? 1 : 0, avoid_dev ? 1 : 0});
+        if (it != g_tune.end() && it->second.choice >= 0) tl_seg_fine = kTuneFine[it->second.choice];
+    }
+    const int rc = fused_launch(MODE_HASF, in_dev, out_dev, n, h, w, 1, r_max, 1, 1, fg, keep_dev, avoid_dev, nullptr,
+                                -1, st, nullptr, reinterpret_cast<int *>(err_dev), nullptr);
+    tl_seg_fine = -1;
+    return rc ?: ok();
 }
 
 int ts_check_device_error(int32_t code) {
@@ -1117,7 +1186,10 @@ int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
 
 int32_t ts_set_segment_stages(int32_t stages) { return g_seg_stages.exchange(stages < 0 ? 0 : stages); }
 
-int32_t ts_set_segment_fine(int32_t stages) { return g_seg_fine.exchange(stages < 0 ? 0 : stages); }
+int32_t ts_set_segment_fine(int32_t stages) {
+    g_seg_fine_fixed.store(1);   // the caller's choice: no tuning
+    return g_seg_fine.exchange(stages < 0 ? 0 : stages);
+}
 
 int32_t ts_set_cluster_teams(int32_t on) { return g_cluster_knob.exchange(on < 0 ? 0 : (on > 2 ? 2 : on)); }
 
