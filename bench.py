@@ -532,6 +532,10 @@ def main():
                                        f"background pixels (W.constraint_masks)"),
                        "parallelism": f"images sharded over {world} GPU(s), no collective",
                        "l2": "flushed between timed steps (256 MiB fill, not timed); per-step CUDA events",
+                       "scheduler": ("library defaults: (segment, image) tasks for batches above one wave; the fine "
+                                     "tail (1 or 2 one-stage segments) chosen by the library from its first three "
+                                     "launches, i.e. inside the warm-up" if not os.environ.get("TS_SEG_FINE") and
+                                     os.environ.get("TS_SEG_TUNE", "1") != "0" else "fine tail fixed by environment"),
                        "plan": {"ctas_per_wave": int(plan[0]), "ctas_per_sm": int(plan[1]),
                                 "smem_bytes": int(plan[2]), "smem_mask": int(plan[3]),
                                 "gws_bytes_per_cta": int(plan[4]), "threads_per_cta": int(plan[5])}},

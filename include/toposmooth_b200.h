@@ -220,7 +220,8 @@ int32_t ts_set_segment_stages(int32_t stages);
  * Unless this is called (or env TS_SEG_FINE is set, or TS_SEG_TUNE=0), the
  * blocking device entry picks 2 or 1 per problem (shape, batch, radii,
  * adjacency, constraints) by timing its own first three launches of it;
- * the outputs do not depend on the segmentation.  Returns the previous value. */
+ * the outputs do not depend on the segmentation.  A negative value returns
+ * to that per-problem tuning.  Returns the previous value. */
 int32_t ts_set_segment_fine(int32_t stages);
 
 /* Tuning / A-B: the segmentation used by the streamed host entry

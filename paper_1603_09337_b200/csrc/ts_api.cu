@@ -1187,8 +1187,12 @@ int32_t ts_set_fused_prep(int32_t on) { return g_fused.exchange(on ? 1 : 0); }
 int32_t ts_set_segment_stages(int32_t stages) { return g_seg_stages.exchange(stages < 0 ? 0 : stages); }
 
 int32_t ts_set_segment_fine(int32_t stages) {
+    if (stages < 0) {   // back to per-problem tuning (the stored tail stays the untuned default)
+        g_seg_fine_fixed.store(0);
+        return g_seg_fine.load();
+    }
     g_seg_fine_fixed.store(1);   // the caller's choice: no tuning
-    return g_seg_fine.exchange(stages < 0 ? 0 : stages);
+    return g_seg_fine.exchange(stages);
 }
 
 int32_t ts_set_cluster_teams(int32_t on) { return g_cluster_knob.exchange(on < 0 ? 0 : (on > 2 ? 2 : on)); }

@@ -505,6 +505,28 @@ def test_segmented_scheduler_forced_vs_oracle(seg, fine):
         lib.ts_set_host_segments(olds[3], 0)
 
 
+def test_fine_tail_tuning_keeps_outputs():
+    """The blocking entry tunes the segmented scheduler's fine tail over its
+    first three launches of a problem (tail 2, 1, 2) and then keeps one: every
+    one of those launches, and the non-blocking entry after them, returns the
+    oracle's images."""
+    lib = _lib.load()
+    old_force = lib.ts_set_segment_force(1)
+    lib.ts_set_segment_fine(-1)   # per-problem tuning on (earlier tests fixed the tail)
+    try:
+        rng = np.random.default_rng(77)
+        imgs = np.stack([random_image(rng, 80, 100, rng.uniform(0.3, 0.7)) for _ in range(7)])
+        want = O.hasf_batch(imgs, 4, 8, threads=7)
+        x = torch.from_numpy(imgs).cuda()
+        for _ in range(5):
+            assert np.array_equal(P.hasf_batch(x, 4).cpu().numpy(), want)
+        y, pending = P.hasf_batch(x, 4, blocking=False)
+        pending.check()
+        assert np.array_equal(y.cpu().numpy(), want)
+    finally:
+        lib.ts_set_segment_force(old_force)
+
+
 # ---- netpbm P4 straight into the device layout, CLI on the device (row f2) ----
 def test_p4_rows_round_trip_ragged_widths():
     lib = _lib.load()
