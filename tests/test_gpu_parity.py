@@ -692,3 +692,22 @@ def test_nccl_single_rank_sharded_gather():
     assert pr.exitcode == 0
     assert np.array_equal(out, O.hasf_batch(imgs, 3, 8))
     assert t == 12.5
+
+
+def test_registered_torch_op():
+    """torch.ops.toposmooth_b200.hasf_batch: the CUDA implementation is the
+    fused kernel, the fake implementation traces shape and dtype."""
+    P.register_torch_ops()
+    P.register_torch_ops()   # idempotent
+    rng = np.random.default_rng(21)
+    imgs = np.stack([random_image(rng, 50, 70, 0.5) for _ in range(3)])
+    x = torch.from_numpy(imgs).cuda()
+    y = torch.ops.toposmooth_b200.hasf_batch(x, 3)
+    assert y.dtype == torch.uint8 and y.is_cuda
+    assert np.array_equal(y.cpu().numpy(), O.hasf_batch(imgs, 3, 8))
+    keep = (imgs & (rng.random(imgs.shape) < 0.05)).astype(np.uint8)
+    y = torch.ops.toposmooth_b200.hasf_batch(x, 2, 4, torch.from_numpy(keep).cuda(), None)
+    assert np.array_equal(y.cpu().numpy(), O.hasf_batch(imgs, 2, 4, keep=keep))
+    with torch._subclasses.fake_tensor.FakeTensorMode():
+        f = torch.ops.toposmooth_b200.hasf_batch(torch.empty((2, 8, 9), dtype=torch.uint8, device="cuda"), 1)
+        assert tuple(f.shape) == (2, 8, 9) and f.dtype == torch.uint8
