@@ -18,7 +18,8 @@ SOURCES = ["ts_hasf_8h.cu", "ts_hasf_4h.cu", "ts_hasf_8g.cu", "ts_hasf_4g.cu", "
            "ts_hasf_4h256.cu", "ts_hasf_8g1024.cu", "ts_hasf_4g1024.cu", "ts_hasf.cu", "ts_edt.cu", "ts_ccl.cu", "ts_p4.cu", "ts_api.cu", "ts_hostpack.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         *os.environ.get("TS_NVCC_EXTRA", "").split()]   # TS_NVCC_EXTRA: extra nvcc flags (A/B builds)
 
 
 def _deps():
