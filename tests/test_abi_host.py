@@ -45,6 +45,19 @@ def test_version_and_limits():
     assert lib.ts_max_radius() == 16   # the fused single-launch path; larger radii run per stage
 
 
+def test_segment_fine_knob_semantics():
+    """ts_set_segment_fine: a value fixes the scheduler's fine tail (and returns
+    the previous one), a negative value returns to per-problem tuning and leaves
+    the stored default alone.  Host state only."""
+    lib = _lib.load()
+    base = lib.ts_set_segment_fine(-1)
+    assert base >= 0
+    assert lib.ts_set_segment_fine(3) == base
+    assert lib.ts_set_segment_fine(-1) == 3
+    assert lib.ts_set_segment_fine(base) == 3
+    assert lib.ts_set_segment_fine(-1) == base
+
+
 def test_connectivity_tables_match_reference():
     z = load_golden("lut")
     assert np.array_equal(P.T8_TABLE, z["T8"]) and np.array_equal(P.T4_TABLE, z["T4"])
