@@ -495,9 +495,9 @@ def main():
     e2e_value = cfg.n * world * e2e_steps / (e2e_ms / 1e3)
     # bytes that actually cross the host link per step (ts_hasf_batch_host):
     # the default streamed entry bit-packs the image and any keep / avoid
-    # planes on the host (32 px per uint32 word) for images up to 1024^2;
-    # otherwise uint8 planes
-    packed = args.host_streaming == 1 and cfg.h * cfg.w <= 1024 * 1024
+    # planes on the host (32 px per uint32 word), team-sized images (> 1024^2)
+    # too unless TS_STREAM_BIG=0; otherwise uint8 planes
+    packed = args.host_streaming == 1 and (cfg.h * cfg.w <= 1024 * 1024 or os.environ.get("TS_STREAM_BIG", "1") != "0")
     planes = 1 + (keep_np is not None) + (avoid_np is not None)   # inputs: image + control images
     link_in = planes * (cfg.n * cfg.h * ((cfg.w + 31) // 32) * 4 if packed else cfg.n * cfg.h * cfg.w)
     link_bytes = cfg.n * cfg.h * ((cfg.w + 31) // 32) * 4 if packed else cfg.n * cfg.h * cfg.w

@@ -1259,7 +1259,10 @@ int ts_hasf_batch_host(const uint8_t *in_host, uint8_t *out_host, int64_t n, int
                getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr ||
                getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr || (lb && lb[0] == '1') || few_queues;
     }();
-    if (!big && !serialised && g_streamed.load() && mo.write && mo.wait && r_max <= kMaxR) {
+    // TS_STREAM_BIG=0: team-sized images through the chunked uint8 pipeline below instead
+    static const bool stream_big = !(getenv("TS_STREAM_BIG") && atoi(getenv("TS_STREAM_BIG")) == 0);
+    if ((!big || (stream_big && g_streamed.load() == 1)) && !serialised && g_streamed.load() && mo.write && mo.wait &&
+        r_max <= kMaxR) {
         if (g_streamed.load() == 1)
             return hasf_host_streamed_packed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);
         return hasf_host_streamed(in_host, out_host, n, h, w, r_max, fg, keep_host, avoid_host, user, mo);

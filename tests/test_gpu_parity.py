@@ -380,7 +380,8 @@ def test_streamed_host_entry_vs_device_path(streaming):
     old = lib.ts_set_host_streaming(streaming)
     try:
         stream = torch.cuda.current_stream().cuda_stream
-        for cfg, start, n in (("c1", 1200, 1), ("c1", 1210, 17), ("c1", 1230, 40), ("c4", 4100, 70)):
+        # (c2: team-sized images, one chunk per image, thread-block cluster teams gated on the chunks)
+        for cfg, start, n in (("c1", 1200, 1), ("c1", 1210, 17), ("c1", 1230, 40), ("c2", 60, 3), ("c4", 4100, 70)):
             c = W.CONFIGS[cfg]
             imgs = W.config_batch(c, start, n)
             adj = P.ADJ_84 if c.fg == 8 else P.ADJ_48
@@ -408,6 +409,17 @@ def test_streamed_host_entry_vs_device_path(streaming):
             out = np.zeros_like(imgs)
             _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, 7, h, w, 2, 4, None, None, stream))
             assert np.array_equal(out, O.hasf_batch(imgs, 2, 4, threads=4)), (streaming, h, w)
+        # team-sized images (> 1024^2) with constraints, and an invalid pixel in the second of them
+        imgs = np.stack([random_image(rng, 1100, 1040, 0.5) for _ in range(2)])
+        keep = (imgs & (rng.random(imgs.shape) < 0.02)).astype(np.uint8)
+        avoid = ((rng.random(imgs.shape) < 0.02) & (imgs == 0)).astype(np.uint8)
+        out = np.zeros_like(imgs)
+        _lib.check(lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, 2, 1100, 1040, 2, 8, keep.ctypes.data,
+                                          avoid.ctypes.data, stream))
+        assert np.array_equal(out, O.hasf_batch(imgs, 2, 8, keep=keep, avoid=avoid, threads=2)), streaming
+        imgs[1, 1000, 1000] = 2
+        rc = lib.ts_hasf_batch_host(imgs.ctypes.data, out.ctypes.data, 2, 1100, 1040, 2, 8, None, None, stream)
+        assert rc == _lib.TS_ERR_VALUE and b"0 or 1" in lib.ts_last_error()
         big = W.config_batch("c1", 1300, 40)
         big[35, 100, 100] = 3   # lands in the third 16-image chunk
         hout = np.zeros_like(big)
