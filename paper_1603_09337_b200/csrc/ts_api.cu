@@ -1064,10 +1064,13 @@ int hasf_host_streamed_packed(const uint8_t *in_host, uint8_t *out_host, int64_t
     uint32_t *ha = avoid_host ? g_stage.in + 2 * g_stage.words : nullptr;
     // pack (and validate) chunk k of the image and the constraint planes
     auto pack_chunk = [&](int64_t i0, int64_t cnt) {
-        bool good = pack_images(in_host + i0 * img, hin + i0 * wimg, cnt, h, w, ww);
-        if (hk) good = pack_images(keep_host + i0 * img, hk + i0 * wimg, cnt, h, w, ww) && good;
-        if (ha) good = pack_images(avoid_host + i0 * img, ha + i0 * wimg, cnt, h, w, ww) && good;
-        return good;
+        if (!hk && !ha) return pack_images(in_host + i0 * img, hin + i0 * wimg, cnt, h, w, ww);
+        const uint8_t *src[3] = {in_host + i0 * img, nullptr, nullptr};   // one parallel region for all planes
+        uint32_t *dst[3] = {hin + i0 * wimg, nullptr, nullptr};
+        int np = 1;
+        if (hk) src[np] = keep_host + i0 * img, dst[np++] = hk + i0 * wimg;
+        if (ha) src[np] = avoid_host + i0 * img, dst[np++] = ha + i0 * wimg;
+        return pack_planes(src, dst, np, cnt, h, w, ww);
     };
     static const bool htrace = getenv("TS_HOST_TRACE") != nullptr;   // debug: host timeline of the call on stderr
     const auto ht0 = std::chrono::steady_clock::now();

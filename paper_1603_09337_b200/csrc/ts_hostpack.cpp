@@ -112,6 +112,28 @@ bool pack_images(const uint8_t *in, uint32_t *out, int64_t n, int h, int w, int 
     return ok != 0;
 }
 
+// the same for up to 3 planes (image, keep, avoid) in ONE parallel region: a
+// chunk of the constrained streamed entry pays one fork / join instead of three
+bool pack_planes(const uint8_t *const *in, uint32_t *const *out, int planes, int64_t n, int h, int w, int ww) {
+    const int64_t rows = n * h, total = rows * planes;
+    const bool avx = have_avx2();
+    int ok = 1;
+#pragma omp parallel for schedule(static) reduction(& : ok) if (total >= 256)
+    for (int64_t t = 0; t < total; ++t) {
+        const int pl = (int)(t / rows);
+        const int64_t r = t - pl * rows;
+        const uint8_t *s = in[pl] + r * (int64_t)w;
+        uint32_t *d = out[pl] + r * (int64_t)ww;
+#if defined(__x86_64__)
+        const bool good = avx ? pack_row_avx2(s, d, w, ww) : pack_row_scalar(s, d, w, ww);
+#else
+        const bool good = pack_row_scalar(s, d, w, ww);
+#endif
+        ok &= good ? 1 : 0;
+    }
+    return ok != 0;
+}
+
 void unpack_images(const uint32_t *in, uint8_t *out, int64_t n, int h, int w, int ww) {
     const int64_t rows = n * h;
     const bool avx = have_avx2();
